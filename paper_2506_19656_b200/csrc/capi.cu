@@ -1,0 +1,49 @@
+// Host-side glue of the C ABI: status strings, last-error, launch checks.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace cvb {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int status, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return status;
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(CV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return CV_OK;
+}
+
+}  // namespace cvb
+
+extern "C" {
+
+int cv_version(void) { return 100; /* 0.1.0 */ }
+
+const char *cv_status_string(int status) {
+  switch (status) {
+    case CV_OK: return "ok";
+    case CV_ERR_ARG: return "invalid argument";
+    case CV_ERR_SHAPE: return "inconsistent shape";
+    case CV_ERR_UNSUPPORTED: return "unsupported by the B200 path";
+    case CV_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char *cv_last_error(void) { return cvb::g_last_error.c_str(); }
+
+int cv_max_channels(void) { return cvb::kMaxC; }
+
+}  // extern "C"

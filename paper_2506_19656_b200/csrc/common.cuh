@@ -1,0 +1,188 @@
+// Shared device helpers for the cvb200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "cvb200.h"
+
+namespace cvb {
+
+// ----------------------------------------------------------------- errors
+void set_last_error(const std::string &msg);
+int fail(int status, const char *fmt, ...);
+int check_launch(const char *what);
+
+// ----------------------------------------------------------------- limits
+constexpr int kMaxC = 32;        // channels per stream handled by one CTA row
+constexpr int kSsimRadius = 5;   // 11x11 window
+constexpr int kSsimTaps = 2 * kSsimRadius + 1;
+
+// threads per CTA for the "thread owns band tid % C" mapping: a multiple of C
+// (and of 32) between 128 and 1024.
+__host__ __device__ inline int threads_for_channels(int C) {
+  int nt = 32 * C;
+  while (nt < 128) nt *= 2;
+  return nt;
+}
+
+// ----------------------------------------------------------------- typed loads
+template <typename T> __device__ __forceinline__ T ldg(const T *p) { return __ldg(p); }
+
+template <typename T> struct is_float_t { static constexpr bool value = false; };
+template <> struct is_float_t<float> { static constexpr bool value = true; };
+template <> struct is_float_t<double> { static constexpr bool value = true; };
+
+// ----------------------------------------------------------------- ordered keys
+// Monotone map double -> u64 so atomicMin/atomicMax on keys order like the
+// doubles (-0.0 canonicalised to +0.0).
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  if (v == 0.0) v = 0.0;
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double d;
+  memcpy(&d, &b, sizeof d);
+  return d;
+#endif
+}
+
+// statistics workspace entry, one per (cube, band)
+struct StatsEntry {
+  unsigned long long min_key;
+  unsigned long long max_key;
+  unsigned long long nan_count;
+  unsigned int lead;   // some t=0 cell of the band is NaN (leading fill used)
+  unsigned int pad;
+};
+
+// Commit per-thread band statistics (band = tid % C; NT = blockDim.x is a
+// multiple of C) into the (cube-local) workspace: block reduce in shared
+// memory, then one ordered-key atomic per band. `scratch` needs
+// NT*(2*sizeof(Acc)+8) bytes and all threads must call this.
+template <typename Acc>
+__device__ void commit_band_stats(Acc mn, Acc mx, unsigned nanc, bool lead, int C,
+                                  StatsEntry *ws_cube, unsigned char *scratch) {
+  const int NT = blockDim.x, tid = threadIdx.x;
+  Acc *smn = reinterpret_cast<Acc *>(scratch);
+  Acc *smx = smn + NT;
+  unsigned *snan = reinterpret_cast<unsigned *>(smx + NT);
+  unsigned *slead = snan + NT;
+  __syncthreads();
+  smn[tid] = mn;
+  smx[tid] = mx;
+  snan[tid] = nanc;
+  slead[tid] = lead ? 1u : 0u;
+  __syncthreads();
+  if (tid < C) {
+    Acc bmn = smn[tid], bmx = smx[tid];
+    unsigned long long bn = 0;
+    unsigned bl = 0;
+    for (int i = tid; i < NT; i += C) {
+      bmn = min(bmn, smn[i]);
+      bmx = max(bmx, smx[i]);
+      bn += snan[i];
+      bl |= slead[i];
+    }
+    StatsEntry *en = ws_cube + tid;
+    if (bmn <= bmx) {
+      atomicMin(&en->min_key, dkey((double)bmn));
+      atomicMax(&en->max_key, dkey((double)bmx));
+    }
+    if (bn) atomicAdd(&en->nan_count, bn);
+    if (bl) atomicOr(&en->lead, 1u);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void flag(uint32_t *err, uint32_t f) {
+  if (err) atomicOr(err, f);
+}
+
+// warp-aggregated flag: one atomic per warp
+__device__ __forceinline__ void flag_warp(uint32_t *err, bool cond, uint32_t f) {
+  unsigned m = __ballot_sync(__activemask(), cond);
+  if (m && (threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) flag(err, f);
+}
+
+// --------------------------------------------------------------- fill lookback
+// Forward-fill value of element `e` at time t of cube `a` when src[t][e] is
+// NaN: walk back inside the current segment, then over the per-segment
+// last-observed map; no observation -> the leading fill constant
+// (cube.py:236-242 semantics).
+template <typename TIn>
+__device__ __forceinline__ float fill_lookback(const TIn *__restrict__ cube, int64_t t,
+                                               int64_t inner, int64_t e, int seg_len,
+                                               const float *__restrict__ seg_last_cube,
+                                               float fill) {
+  const int64_t seg = t / seg_len;
+  const int64_t t_lo = seg * seg_len;
+  for (int64_t u = t - 1; u >= t_lo; --u) {
+    float v = (float)cube[u * inner + e];
+    if (!isnan(v)) return v;
+  }
+  for (int64_t s = seg - 1; s >= 0; --s) {
+    float v = seg_last_cube[s * inner + e];
+    if (!isnan(v)) return v;
+  }
+  return fill;
+}
+
+// ----------------------------------------------------------------- quantiser
+// Per-band constants of quantize (transform.py:89-101).
+struct QBand {
+  double m, M, s, r, L;
+  bool constant;
+};
+
+__device__ __forceinline__ QBand make_qband(double m, double M, int bit_depth) {
+  QBand q;
+  q.m = m;
+  q.M = M;
+  double span = __dsub_rn(M, m);
+  q.constant = (span == 0.0);
+  q.s = q.constant ? 1.0 : span;
+  q.r = __drcp_rn(q.s);
+  q.L = (double)((1u << bit_depth) - 1u);
+  return q;
+}
+
+// q = floor(((v - m) / s) * L + 0.5) exactly as IEEE float64 evaluates it in
+// the reference. Fast path: multiply by the rounded reciprocal; its result is
+// within 6 ulp(L) (< 5e-11) of the reference x, so whenever x+0.5 is more than
+// 2^-28 away from an integer both floors agree. Otherwise recompute with the
+// correctly-rounded division in the reference's operation order.
+__device__ __forceinline__ uint32_t quantize_value(double v, const QBand &b) {
+  const double diff = __dsub_rn(v, b.m);
+  double x = __dmul_rn(__dmul_rn(diff, b.r), b.L);
+  double t = __dadd_rn(x, 0.5);
+  double q = floor(t);
+  double fr = __dsub_rn(t, q);
+  const double eps = 3.725290298461914e-09;  // 2^-28
+  if (fr < eps || fr > 1.0 - eps) {
+    x = __dmul_rn(__ddiv_rn(diff, b.s), b.L);
+    q = floor(__dadd_rn(x, 0.5));
+  }
+  if (b.constant) q = 0.0;
+  // out-of-range values are flagged by the caller; keep the cast defined
+  q = fmin(fmax(q, 0.0), 65535.0);
+  return (uint32_t)q;
+}
+
+// dequantize (transform.py:122-125): min + (q / L) * (max - min)
+__device__ __forceinline__ double dequantize_value(uint32_t q, double m, double span, double L,
+                                                   bool constant) {
+  if (constant) return m;
+  return __dadd_rn(m, __dmul_rn(__ddiv_rn((double)q, L), span));
+}
+
+}  // namespace cvb

@@ -1,0 +1,392 @@
+// K2/K3 — band PCA: fp64 shifted Gram (+ band stats), projection (+ component
+// stats) and inverse projection.
+//
+// Replaces, for the array path:
+//   pca_fit (covariance)  /root/reference/pkg/src/cubevid/transform.py:172-179
+//   pca_forward           /root/reference/pkg/src/cubevid/transform.py:191-199
+//   fit_quant on the PCs  SPEC.md:229 (transform.py:61-70)
+//   pca_inverse           /root/reference/pkg/src/cubevid/transform.py:202-210
+// The eigendecomposition (transform.py:180-187) stays on the host (C x C).
+#include "common.cuh"
+#include "pca_params.cuh"
+
+namespace cvb {
+
+constexpr int kGramK = 4;  // elements per thread per chunk
+
+// Gram partial of one CTA over a grid-stride set of pixel chunks.
+// Staging: thread-owns-elements (band tid % C) -> shifted f64 in smem;
+// accumulation: 4x4 tiles of the upper block triangle, one tile per thread,
+// pixels strided over the lanes sharing a tile.
+template <typename TIn>
+__global__ void __launch_bounds__(1024)
+k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ partials,
+       StatsEntry *__restrict__ stats, uint32_t *err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int P = NT * kGramK / C;
+  const int CS = C + 1;  // padded row stride
+  double *xs = reinterpret_cast<double *>(smem);  // [P][CS]
+  const int nb = (C + 3) / 4;
+  const int ntile = nb * (nb + 1) / 2;
+  const int nlanes = NT / ntile;
+  // tile of this thread
+  const int my_tile = tid % ntile, my_lane = tid / ntile;
+  int bi = 0, bj = 0;
+  {
+    int tt = my_tile;
+    for (int i = 0; i < nb; ++i) {
+      const int row = nb - i;
+      if (tt < row) { bi = i; bj = i + tt; break; }
+      tt -= row;
+    }
+  }
+  const bool tile_active = my_lane < nlanes;
+  const int c = tid % C;
+  const double shift = (double)ldg(src + c);
+
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
+  double bsum = 0.0;
+  float mn = INFINITY, mx = -INFINITY;
+  double mnd = INFINITY, mxd = -INFINITY;
+  bool nonfinite = false, isn = false;
+
+  const int64_t nchunks = (n_pix + P - 1) / P;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t pix0 = ch * P;
+    const int64_t e0 = pix0 * C;
+    const int64_t ne = n_pix * C;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kGramK; ++k) {
+      const int el = tid + k * NT;
+      const int64_t e = e0 + el;
+      double d = 0.0;
+      if (e < ne) {
+        const TIn v = ldg(src + e);
+        const double vd = (double)v;
+        if constexpr (is_float_t<TIn>::value) {
+          if (isnan(v)) isn = true;
+          else if (isinf(v)) nonfinite = true;
+        }
+        mnd = fmin(mnd, vd);
+        mxd = fmax(mxd, vd);
+        d = __dsub_rn(vd, shift);
+        if (isfinite(d)) bsum = __dadd_rn(bsum, d);
+      }
+      xs[(el / C) * CS + (el % C)] = isfinite(d) ? d : 0.0;
+    }
+    __syncthreads();
+    if (tile_active) {
+      const int lim = (int)min((int64_t)P, n_pix - pix0);
+      for (int p = my_lane; p < lim; p += nlanes) {
+        double rv[4], cv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int ci = 4 * bi + r, cj = 4 * bj + r;
+          rv[r] = ci < C ? xs[p * CS + ci] : 0.0;
+          cv[r] = cj < C ? xs[p * CS + cj] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) acc[r][s] = __fma_rn(rv[r], cv[s], acc[r][s]);
+      }
+    }
+  }
+  flag_warp(err, nonfinite, CV_FLAG_NONFINITE);
+  flag_warp(err, isn, CV_FLAG_NAN);
+  (void)mn;
+  (void)mx;
+
+  // band stats
+  if (stats) commit_band_stats<double>(mnd, mxd, 0u, false, C, stats, smem);
+
+  // deterministic CTA reduction of the tiles: red[lane][tile][16]
+  __syncthreads();
+  double *red = reinterpret_cast<double *>(smem);
+  if (tile_active) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) red[((size_t)my_lane * ntile + my_tile) * 16 + r * 4 + s] = acc[r][s];
+  }
+  __syncthreads();
+  const int stride = C + C * C;
+  double *part = partials + (size_t)blockIdx.x * stride;
+  for (int idx = tid; idx < ntile * 16; idx += NT) {
+    const int tl = idx / 16, rs = idx % 16;
+    double sum = 0.0;
+    for (int l = 0; l < nlanes; ++l) sum += red[((size_t)l * ntile + tl) * 16 + rs];
+    int tbi = 0, tbj = 0, tt = tl;
+    for (int i = 0; i < nb; ++i) {
+      const int row = nb - i;
+      if (tt < row) { tbi = i; tbj = i + tt; break; }
+      tt -= row;
+    }
+    const int ci = 4 * tbi + rs / 4, cj = 4 * tbj + rs % 4;
+    if (ci < C && cj < C) {
+      part[C + ci * C + cj] = sum;
+      part[C + cj * C + ci] = sum;
+    }
+  }
+  __syncthreads();
+  // band sums: threads sharing band c
+  red[tid] = bsum;
+  __syncthreads();
+  if (tid < C) {
+    double s = 0.0;
+    for (int i = tid; i < NT; i += C) s += red[i];
+    part[tid] = s;
+  }
+}
+
+__global__ void k_reduce_partials(const double *__restrict__ partials, int nparts, int stride,
+                                  double *__restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= stride) return;
+  double s = 0.0;
+  for (int p = 0; p < nparts; ++p) s += partials[(size_t)p * stride + i];
+  out[i] = s;
+}
+
+// Projection: stage spectra (thread-owns-elements), then one thread per pixel
+// computes the K components; per-component min/max kept in registers (KB >= K).
+template <typename TIn, typename TO, int KB>
+__global__ void __launch_bounds__(1024)
+k_pca_project(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
+              StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int C = pca.C, K = pca.K;
+  const int P = NT * kGramK / C;
+  const int CS = C + 1;
+  double *xs = reinterpret_cast<double *>(smem);
+  const int64_t a = blockIdx.y;
+  const TIn *cube = src + a * n_pix * C;
+  double mn[KB], mx[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    mn[j] = INFINITY;
+    mx[j] = -INFINITY;
+  }
+  bool bad = false;
+  const int64_t nchunks = (n_pix + P - 1) / P;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t pix0 = ch * P;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kGramK; ++k) {
+      const int el = tid + k * NT;
+      const int64_t e = pix0 * C + el;
+      double v = 0.0;
+      if (e < n_pix * C) {
+        v = (double)ldg(cube + e);
+        bad |= !isfinite(v);
+      }
+      xs[(el / C) * CS + (el % C)] = v;
+    }
+    __syncthreads();
+    for (int p = tid; p < P; p += NT) {
+      const int64_t pix = pix0 + p;
+      if (pix >= n_pix) break;
+      double d[kMaxC];
+#pragma unroll
+      for (int c = 0; c < kMaxC; ++c)
+        if (c < C) d[c] = __dsub_rn(xs[p * CS + c], pca.mean[c]);
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        if (j < K) {
+          const double pc = project_one(d, pca, j);
+          mn[j] = fmin(mn[j], pc);
+          mx[j] = fmax(mx[j], pc);
+          if (out) out[(a * n_pix + pix) * K + j] = (TO)pc;
+        }
+      }
+    }
+  }
+  flag_warp(err, bad, CV_FLAG_NONFINITE);
+  if (stats) {
+    // reduce per component: warp shuffle then one atomic per warp and component
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      if (j < K) {
+        double a_mn = mn[j], a_mx = mx[j];
+        for (int o = 16; o > 0; o >>= 1) {
+          a_mn = fmin(a_mn, __shfl_xor_sync(0xffffffffu, a_mn, o));
+          a_mx = fmax(a_mx, __shfl_xor_sync(0xffffffffu, a_mx, o));
+        }
+        if ((tid & 31) == 0 && a_mn <= a_mx) {
+          atomicMin(&stats[a * K + j].min_key, dkey(a_mn));
+          atomicMax(&stats[a * K + j].max_key, dkey(a_mx));
+        }
+      }
+    }
+  }
+}
+
+// Inverse projection: one thread per pixel.
+template <typename TIn, typename TO>
+__global__ void __launch_bounds__(256)
+k_pca_inverse(const TIn *__restrict__ pc, int64_t n_total_pix, TO *__restrict__ out,
+              const PcaParams pca) {
+  const int C = pca.C, K = pca.K;
+  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < n_total_pix;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    double v[kMaxC];
+#pragma unroll
+    for (int j = 0; j < kMaxC; ++j)
+      if (j < K) v[j] = (double)ldg(pc + pix * K + j);
+    for (int c = 0; c < C; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < kMaxC; ++j)
+        if (j < K) acc = __fma_rn(v[j], pca.W[j * kMaxC + c], acc);
+      out[pix * C + c] = (TO)__dadd_rn(acc, pca.mean[c]);
+    }
+  }
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int gram_blocks(int64_t n_pix, int C) {
+  const int NT = threads_for_channels(C);
+  const int P = NT * kGramK / C;
+  const int64_t nchunks = (n_pix + P - 1) / P;
+  int64_t nb = 2 * (int64_t)num_sms();
+  if (nb > nchunks) nb = nchunks;
+  if (nb < 1) nb = 1;
+  return (int)nb;
+}
+
+template <typename TIn>
+static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *out, void *stats,
+                       uint32_t *err, cudaStream_t st) {
+  const int NT = threads_for_channels(C);
+  const int P = NT * kGramK / C;
+  const int nb = (C + 3) / 4, ntile = nb * (nb + 1) / 2;
+  size_t sm = (size_t)P * (C + 1) * sizeof(double);
+  size_t sm2 = (size_t)NT * 16 * sizeof(double);  // tile reduction (>= ntile*nlanes*16)
+  (void)ntile;
+  if (sm2 > sm) sm = sm2;
+  const int nblk = gram_blocks(n_pix, C);
+  auto kern = k_gram<TIn>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  kern<<<nblk, NT, sm, st>>>((const TIn *)src, n_pix, C, (double *)ws, (StatsEntry *)stats, err);
+  int s = check_launch("cv_pca_gram");
+  if (s != CV_OK) return s;
+  const int stride = C + C * C;
+  k_reduce_partials<<<(stride + 255) / 256, 256, 0, st>>>((const double *)ws, nblk, stride, out);
+  return check_launch("cv_pca_gram(reduce)");
+}
+
+template <typename TIn, typename TO>
+static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const PcaParams &p,
+                          void *out, void *stats, uint32_t *err, cudaStream_t st) {
+  const int NT = threads_for_channels(p.C);
+  const int P = NT * kGramK / p.C;
+  const size_t sm = (size_t)P * (p.C + 1) * sizeof(double);
+  const int64_t nchunks = (n_pix + P - 1) / P;
+  int64_t nb = 4 * (int64_t)num_sms() / (n_cubes > 0 ? n_cubes : 1);
+  if (nb < 1) nb = 1;
+  if (nb > nchunks) nb = nchunks;
+  dim3 grid((unsigned)nb, (unsigned)n_cubes);
+#define CV_PROJ(KB)                                                                               \
+  do {                                                                                            \
+    auto kern = k_pca_project<TIn, TO, KB>;                                                       \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    kern<<<grid, NT, sm, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);  \
+  } while (0)
+  if (p.K <= 4) CV_PROJ(4);
+  else if (p.K <= 8) CV_PROJ(8);
+  else if (p.K <= 16) CV_PROJ(16);
+  else CV_PROJ(32);
+#undef CV_PROJ
+  return check_launch("cv_pca_project");
+}
+
+}  // namespace cvb
+
+using namespace cvb;
+
+extern "C" {
+
+size_t cv_gram_ws_bytes(int64_t n_pix, int32_t C) {
+  if (C <= 0) return 0;
+  return (size_t)gram_blocks(n_pix, C) * (size_t)(C + C * C) * sizeof(double);
+}
+
+int cv_pca_gram(const void *src, int32_t dtype, int64_t n_pix, int32_t C, void *ws, double *out,
+                void *stats_ws, uint32_t *err_word, void *stream) {
+  if (!src || !ws || !out) return fail(CV_ERR_ARG, "cv_pca_gram: null pointer");
+  if (C <= 0 || C > kMaxC) return fail(CV_ERR_UNSUPPORTED, "cv_pca_gram: %d channels (supported 1..%d)", C, kMaxC);
+  if (n_pix <= 0) return fail(CV_ERR_SHAPE, "cv_pca_gram: no pixels");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (dtype) {
+    case CV_F32: return launch_gram<float>(src, n_pix, C, ws, out, stats_ws, err_word, st);
+    case CV_F64: return launch_gram<double>(src, n_pix, C, ws, out, stats_ws, err_word, st);
+    case CV_U16: return launch_gram<uint16_t>(src, n_pix, C, ws, out, stats_ws, err_word, st);
+    case CV_U8: return launch_gram<uint8_t>(src, n_pix, C, ws, out, stats_ws, err_word, st);
+    default: return fail(CV_ERR_ARG, "cv_pca_gram: unknown dtype %d", dtype);
+  }
+}
+
+int cv_pca_project(const void *src, int32_t dtype, int64_t n_cubes, int64_t n_pix, int32_t C,
+                   const double *mean, const double *comps, int32_t K, void *out, int32_t out_dtype,
+                   void *stats_ws, uint32_t *err_word, void *stream) {
+  if (!src) return fail(CV_ERR_ARG, "cv_pca_project: null source");
+  PcaParams p;
+  int s = make_pca_params(p, mean, comps, K, C);
+  if (s != CV_OK) return s;
+  if (n_cubes < 0 || n_pix < 0 || n_cubes > 65535) return fail(CV_ERR_SHAPE, "cv_pca_project: bad sizes");
+  if (n_cubes == 0 || n_pix == 0) return CV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool f64 = out_dtype == CV_F64;
+  if (out && out_dtype != CV_F32 && out_dtype != CV_F64) return fail(CV_ERR_ARG, "cv_pca_project: out must be f32/f64");
+  switch (dtype) {
+    case CV_F32: return f64 ? launch_project<float, double>(src, n_cubes, n_pix, p, out, stats_ws, err_word, st)
+                            : launch_project<float, float>(src, n_cubes, n_pix, p, out, stats_ws, err_word, st);
+    case CV_F64: return f64 ? launch_project<double, double>(src, n_cubes, n_pix, p, out, stats_ws, err_word, st)
+                            : launch_project<double, float>(src, n_cubes, n_pix, p, out, stats_ws, err_word, st);
+    case CV_U16: return f64 ? launch_project<uint16_t, double>(src, n_cubes, n_pix, p, out, stats_ws, err_word, st)
+                            : launch_project<uint16_t, float>(src, n_cubes, n_pix, p, out, stats_ws, err_word, st);
+    default: return fail(CV_ERR_ARG, "cv_pca_project: unsupported dtype %d", dtype);
+  }
+}
+
+int cv_pca_inverse(const void *pc, int32_t dtype, int64_t n_cubes, int64_t n_pix, int32_t K,
+                   const double *mean, const double *comps, int32_t C, void *out, int32_t out_dtype,
+                   void *stream) {
+  if (!pc || !out) return fail(CV_ERR_ARG, "cv_pca_inverse: null pointer");
+  PcaParams p;
+  int s = make_pca_params(p, mean, comps, K, C);
+  if (s != CV_OK) return s;
+  const int64_t n = n_cubes * n_pix;
+  if (n <= 0) return CV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nb = (n + 255) / 256;
+  if (nb > 148 * 32) nb = 148 * 32;
+#define CV_INV(TI, TO) k_pca_inverse<TI, TO><<<(unsigned)nb, 256, 0, st>>>((const TI *)pc, n, (TO *)out, p)
+  if (dtype == CV_F32 && out_dtype == CV_F32) CV_INV(float, float);
+  else if (dtype == CV_F32 && out_dtype == CV_F64) CV_INV(float, double);
+  else if (dtype == CV_F64 && out_dtype == CV_F32) CV_INV(double, float);
+  else if (dtype == CV_F64 && out_dtype == CV_F64) CV_INV(double, double);
+  else return fail(CV_ERR_ARG, "cv_pca_inverse: dtypes must be f32/f64");
+#undef CV_INV
+  return check_launch("cv_pca_inverse");
+}
+
+}  // extern "C"

@@ -1,0 +1,385 @@
+// K4 — quantisation into integer frames, and K5a — dequantisation.
+//
+// Replaces, for the array path:
+//   quantize            /root/reference/pkg/src/cubevid/transform.py:77-105
+//   pack_groups         /root/reference/pkg/src/cubevid/plan.py:118-128
+//   _frames_to_planar_bytes / _planar_bytes_to_frames
+//                       /root/reference/pkg/src/cubevid/codecs/bridge.py:157-174
+//   pca_forward (fused) /root/reference/pkg/src/cubevid/transform.py:191-199
+//   dequantize          /root/reference/pkg/src/cubevid/transform.py:108-126
+//
+// k_quantize uses the stats kernel's "column chunk x time segment"
+// decomposition: a CTA owns P pixels (NT*4 elements, NT a multiple of C) for
+// seg_len time steps. Each step is one coalesced sweep of the source chunk;
+// the forward-fill carry of every owned element stays in registers; the
+// segment's first carry comes from the per-segment last-observed map. Planar
+// output is staged in shared memory and written as 16-byte vectors per plane.
+#include "common.cuh"
+#include "pca_params.cuh"
+
+namespace cvb {
+
+constexpr int kQK = 4;  // elements per thread per time step
+
+template <typename TIn> struct StageT { using type = float; };
+template <> struct StageT<double> { using type = double; };
+
+int make_pca_params(PcaParams &p, const double *mean, const double *comps, int K, int C) {
+  if (!mean || !comps) return fail(CV_ERR_ARG, "PCA model pointers are null");
+  if (C <= 0 || C > kMaxC || K <= 0 || K > C)
+    return fail(CV_ERR_ARG, "PCA model shape K=%d C=%d unsupported (C <= %d, 1 <= K <= C)", K, C, kMaxC);
+  memset(&p, 0, sizeof p);
+  p.C = C;
+  p.K = K;
+  for (int c = 0; c < C; ++c) p.mean[c] = mean[c];
+  for (int j = 0; j < K; ++j)
+    for (int c = 0; c < C; ++c) p.W[j * kMaxC + c] = comps[j * C + c];
+  return CV_OK;
+}
+
+struct QuantArgs {
+  int64_t T, HW;
+  int C, E, G;
+  int bit_depth, clamp, pad_mode;
+  float fill;
+  int seg_len;
+  const double *mins, *maxs;
+  const float *seg_last;
+  uint32_t *err;
+};
+
+// Range check + clamp on the float64 value (transform.py:92-97).
+__device__ __forceinline__ double range_prep(double v, const QBand &b, int clamp, bool &bad) {
+  if (clamp) return fmin(fmax(v, b.m), b.M);
+  bad |= (v < b.m) || (v > b.M) || isnan(v);
+  return v;
+}
+
+template <typename TIn, typename TOut, bool PCA, bool PLANAR, bool FILL>
+__global__ void __launch_bounds__(1024)
+k_quantize(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs args,
+           const PcaParams pca) {
+  using S = typename StageT<TIn>::type;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x;
+  const int tid = threadIdx.x;
+  const int C = args.C, E = args.E;
+  const int64_t T = args.T, HW = args.HW;
+  const int64_t inner = HW * C;
+  const int P = NT * kQK / C;  // pixels per chunk
+  const int64_t a = blockIdx.z;
+  const int64_t seg = blockIdx.y;
+  const int64_t nseg = gridDim.y;
+  const int64_t pix0 = (int64_t)blockIdx.x * P;
+  const int64_t e0 = pix0 * C + tid;
+  const int64_t t0 = seg * args.seg_len;
+  const int64_t t1 = min(T, t0 + (int64_t)args.seg_len);
+  const TIn *cube = src + a * T * inner;
+
+  // shared memory carve-up
+  S *xs = reinterpret_cast<S *>(smem);                                   // [P][C+1] (PCA)
+  size_t off = PCA ? (size_t)P * (C + 1) * sizeof(S) : 0;
+  off = (off + 15) & ~(size_t)15;
+  TOut *sq = reinterpret_cast<TOut *>(smem + off);                       // [2][E][P] (PLANAR)
+  off += PLANAR ? 2 * (size_t)E * P * sizeof(TOut) : 0;
+  off = (off + 15) & ~(size_t)15;
+  QBand *qbs = reinterpret_cast<QBand *>(smem + off);                    // [E] (PCA)
+  if constexpr (PCA) {
+    for (int j = tid; j < E; j += NT)
+      qbs[j] = make_qband(args.mins[a * E + j], args.maxs[a * E + j], args.bit_depth);
+    __syncthreads();
+  }
+
+  // per-thread quantiser for the non-PCA path: band = tid % C
+  QBand qb;
+  if constexpr (!PCA) {
+    const int c = tid % C;
+    qb = make_qband(args.mins[a * E + c], args.maxs[a * E + c], args.bit_depth);
+  }
+
+  // forward-fill carries for the owned elements
+  float carry[kQK];
+  if constexpr (FILL) {
+    const float *sl = args.seg_last + a * nseg * inner;
+#pragma unroll
+    for (int k = 0; k < kQK; ++k) {
+      const int64_t e = e0 + (int64_t)k * NT;
+      carry[k] = args.fill;
+      if (e < inner) {
+        for (int64_t s = seg - 1; s >= 0; --s) {
+          float v = sl[s * inner + e];
+          if (!isnan(v)) {
+            carry[k] = v;
+            break;
+          }
+        }
+      }
+    }
+  }
+
+  bool bad = false;
+  bool nanbad = false;
+  const bool full_chunk = (pix0 + P <= HW);
+  int buf = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const TIn *row = cube + t * inner;
+    S v[kQK];
+#pragma unroll
+    for (int k = 0; k < kQK; ++k) {
+      const int64_t e = e0 + (int64_t)k * NT;
+      v[k] = (e < inner) ? (S)ldg(row + e) : (S)0;
+    }
+    if constexpr (FILL) {
+#pragma unroll
+      for (int k = 0; k < kQK; ++k) {
+        if (isnan(v[k])) v[k] = (S)carry[k];
+        else carry[k] = (float)v[k];
+      }
+    }
+    if constexpr (!PCA) {
+#pragma unroll
+      for (int k = 0; k < kQK; ++k) {
+        const int64_t el = (int64_t)tid + (int64_t)k * NT;  // element index inside the chunk
+        const int64_t e = e0 + (int64_t)k * NT;
+        if (e >= inner) continue;
+        if constexpr (!FILL) nanbad |= isnan((double)v[k]);
+        const double d = range_prep((double)v[k], qb, args.clamp, bad);
+        const uint32_t q = quantize_value(d, qb);
+        if constexpr (PLANAR) {
+          const int p = (int)(el / C), c = (int)(el % C);
+          sq[((size_t)buf * E + c) * P + p] = (TOut)q;
+        } else {
+          out[(a * T + t) * inner + e] = (TOut)q;
+        }
+      }
+    } else {
+      // stage the (filled) spectra, then one thread per pixel projects
+#pragma unroll
+      for (int k = 0; k < kQK; ++k) {
+        const int el = tid + k * NT;
+        const int p = el / C, c = el % C;
+        if constexpr (!FILL) nanbad |= isnan((double)v[k]);
+        xs[p * (C + 1) + c] = v[k];
+      }
+      __syncthreads();
+      for (int p = tid; p < P; p += NT) {
+        const int64_t pix = pix0 + p;
+        if (pix >= HW) break;
+        double d[kMaxC];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c)
+          if (c < C) d[c] = __dsub_rn((double)xs[p * (C + 1) + c], pca.mean[c]);
+        for (int j = 0; j < E; ++j) {
+          const double pc = project_one(d, pca, j);
+          const QBand b = qbs[j];
+          const double dv = range_prep(pc, b, args.clamp, bad);
+          const uint32_t q = quantize_value(dv, b);
+          if constexpr (PLANAR) sq[((size_t)buf * E + j) * P + p] = (TOut)q;
+          else out[((a * T + t) * HW + pix) * E + j] = (TOut)q;
+        }
+      }
+    }
+    if constexpr (PLANAR || PCA) __syncthreads();
+    if constexpr (PLANAR) {
+      // planes of this time step: frames[a][g][t][jp][pix0 .. pix0+P)
+      const int nplanes = 3 * args.G;
+      const TOut *sb = sq + (size_t)buf * E * P;
+      constexpr int VEC = 16 / sizeof(TOut);
+      const bool vec_ok = full_chunk && ((HW * (int64_t)sizeof(TOut)) % 16 == 0) && (P % VEC == 0);
+      if (vec_ok) {
+        const int nv = P / VEC;
+        for (int i = tid; i < nplanes * nv; i += NT) {
+          const int pl = i / nv, vi = i % nv;
+          const int g = pl / 3, jp = pl % 3;
+          TOut *dst = out + (((a * args.G + g) * T + t) * 3 + jp) * HW + pix0 + (int64_t)vi * VEC;
+          uint4 val = make_uint4(0, 0, 0, 0);
+          if (pl < E || args.pad_mode == CV_PAD_REPEAT) {
+            const int sp = pl < E ? pl : E - 1;
+            val = *reinterpret_cast<const uint4 *>(sb + (size_t)sp * P + (size_t)vi * VEC);
+          }
+          *reinterpret_cast<uint4 *>(dst) = val;
+        }
+      } else {
+        for (int i = tid; i < nplanes * P; i += NT) {
+          const int pl = i / P, p = i % P;
+          if (pix0 + p >= HW) continue;
+          const int g = pl / 3, jp = pl % 3;
+          TOut val = 0;
+          if (pl < E || args.pad_mode == CV_PAD_REPEAT) val = sb[(size_t)(pl < E ? pl : E - 1) * P + p];
+          out[(((a * args.G + g) * T + t) * 3 + jp) * HW + pix0 + p] = val;
+        }
+      }
+      buf ^= 1;
+    }
+  }
+  flag_warp(args.err, bad, CV_FLAG_RANGE);
+  flag_warp(args.err, nanbad, CV_FLAG_NAN);
+}
+
+// dequantize: channel-last or planar integer frames -> channel-last values.
+template <typename TQ, typename TO, bool PLANAR>
+__global__ void __launch_bounds__(256)
+k_dequantize(const TQ *__restrict__ q, TO *__restrict__ out, int64_t n_total, int64_t T, int64_t HW,
+             int E, int G, const double *__restrict__ mins, const double *__restrict__ maxs,
+             int bit_depth, int64_t n_cubes, uint32_t *err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *sm = reinterpret_cast<double *>(smem);  // [n_cubes*E] mins, spans when small
+  const double L = (double)((1u << bit_depth) - 1u);
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % E);
+    const int64_t pixel = i / E;  // (a*T + t)*HW + pix
+    const int64_t a = pixel / (T * HW);
+    uint32_t qv;
+    if constexpr (PLANAR) {
+      const int64_t rem = pixel - a * T * HW;
+      const int64_t t = rem / HW, pix = rem % HW;
+      qv = (uint32_t)q[(((a * G + c / 3) * T + t) * 3 + c % 3) * HW + pix];
+    } else {
+      qv = (uint32_t)q[i];
+    }
+    bad |= (double)qv > L;
+    const double m = mins[a * E + c], M = maxs[a * E + c];
+    const double span = __dsub_rn(M, m);
+    out[i] = (TO)dequantize_value(qv, m, span, L, span == 0.0);
+  }
+  flag_warp(err, bad, CV_FLAG_INT_RANGE);
+  (void)sm;
+  (void)n_cubes;
+}
+
+template <typename TIn, typename TOut, bool PCA, bool PLANAR, bool FILL>
+static int launch_q(const void *src, void *out, const QuantArgs &args, const PcaParams &pca,
+                    int64_t n_cubes, cudaStream_t st) {
+  using S = typename StageT<TIn>::type;
+  const int NT = threads_for_channels(args.C);
+  const int P = NT * kQK / args.C;
+  size_t sm = 0;
+  if (PCA) sm += (size_t)P * (args.C + 1) * sizeof(S);
+  sm = (sm + 15) & ~(size_t)15;
+  if (PLANAR) sm += 2 * (size_t)args.E * P * sizeof(TOut);
+  sm = (sm + 15) & ~(size_t)15;
+  if (PCA) sm += (size_t)args.E * sizeof(QBand);
+  auto kern = k_quantize<TIn, TOut, PCA, PLANAR, FILL>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((unsigned)((args.HW + P - 1) / P), (unsigned)cv_num_segments(args.T, args.seg_len),
+            (unsigned)n_cubes);
+  kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);
+  return check_launch("cv_quantize");
+}
+
+template <typename TIn, typename TOut>
+static int dispatch_q2(const void *src, void *out, const QuantArgs &a, const PcaParams &p,
+                       int64_t n, cudaStream_t st, bool pca, bool planar, bool fill) {
+  if (pca) {
+    if (planar) return fill ? launch_q<TIn, TOut, true, true, true>(src, out, a, p, n, st)
+                            : launch_q<TIn, TOut, true, true, false>(src, out, a, p, n, st);
+    return fill ? launch_q<TIn, TOut, true, false, true>(src, out, a, p, n, st)
+                : launch_q<TIn, TOut, true, false, false>(src, out, a, p, n, st);
+  }
+  if (planar) return fill ? launch_q<TIn, TOut, false, true, true>(src, out, a, p, n, st)
+                          : launch_q<TIn, TOut, false, true, false>(src, out, a, p, n, st);
+  return fill ? launch_q<TIn, TOut, false, false, true>(src, out, a, p, n, st)
+              : launch_q<TIn, TOut, false, false, false>(src, out, a, p, n, st);
+}
+
+template <typename TIn>
+static int dispatch_q1(const void *src, void *out, const QuantArgs &a, const PcaParams &p,
+                       int64_t n, cudaStream_t st, bool pca, bool planar, bool fill) {
+  if (a.bit_depth == 8) return dispatch_q2<TIn, uint8_t>(src, out, a, p, n, st, pca, planar, fill);
+  return dispatch_q2<TIn, uint16_t>(src, out, a, p, n, st, pca, planar, fill);
+}
+
+static bool valid_depth(int b) { return b == 8 || b == 10 || b == 12 || b == 16; }
+
+}  // namespace cvb
+
+using namespace cvb;
+
+extern "C" {
+
+int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int64_t HW, int32_t C,
+                const double *mins, const double *maxs, int32_t bit_depth, int32_t clamp,
+                int32_t fill_mode, float fill_value, int32_t seg_len, const float *seg_last,
+                const double *pca_mean, const double *pca_comps, int32_t n_pcs, int32_t out_layout,
+                int32_t pad_mode, void *out, uint32_t *err_word, void *stream) {
+  if (!src || !out || !mins || !maxs) return fail(CV_ERR_ARG, "cv_quantize: null pointer");
+  if (!valid_depth(bit_depth)) return fail(CV_ERR_ARG, "bit depth %d not in (8, 10, 12, 16)", bit_depth);
+  if (C <= 0 || C > kMaxC) return fail(CV_ERR_UNSUPPORTED, "cv_quantize: %d channels (supported 1..%d)", C, kMaxC);
+  if (n_cubes < 0 || T < 0 || HW < 0) return fail(CV_ERR_SHAPE, "cv_quantize: negative size");
+  if (seg_len <= 0) return fail(CV_ERR_ARG, "cv_quantize: seg_len must be positive");
+  if (n_cubes > 65535 || cv_num_segments(T, seg_len) > 65535)
+    return fail(CV_ERR_UNSUPPORTED, "cv_quantize: grid too large");
+  const bool pca = pca_comps != nullptr;
+  const bool fill = fill_mode != 0;
+  if (fill && (dtype != CV_F32 || !seg_last))
+    return fail(CV_ERR_ARG, "cv_quantize: fill_mode needs f32 input and a seg_last map");
+  if (out_layout != CV_LAYOUT_CHANNEL_LAST && out_layout != CV_LAYOUT_PLANAR)
+    return fail(CV_ERR_ARG, "cv_quantize: unknown layout %d", out_layout);
+  PcaParams p;
+  memset(&p, 0, sizeof p);
+  int E = C;
+  if (pca) {
+    int s = make_pca_params(p, pca_mean, pca_comps, n_pcs, C);
+    if (s != CV_OK) return s;
+    E = n_pcs;
+  }
+  if (n_cubes == 0 || T == 0 || HW == 0) return CV_OK;
+  QuantArgs a;
+  a.T = T;
+  a.HW = HW;
+  a.C = C;
+  a.E = E;
+  a.G = (E + 2) / 3;
+  a.bit_depth = bit_depth;
+  a.clamp = clamp;
+  a.pad_mode = pad_mode;
+  a.fill = fill_value;
+  a.seg_len = seg_len;
+  a.mins = mins;
+  a.maxs = maxs;
+  a.seg_last = seg_last;
+  a.err = err_word;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool planar = out_layout == CV_LAYOUT_PLANAR;
+  switch (dtype) {
+    case CV_F32: return dispatch_q1<float>(src, out, a, p, n_cubes, st, pca, planar, fill);
+    case CV_F64: return dispatch_q1<double>(src, out, a, p, n_cubes, st, pca, planar, false);
+    case CV_U16: return dispatch_q1<uint16_t>(src, out, a, p, n_cubes, st, pca, planar, false);
+    case CV_U8: return dispatch_q1<uint8_t>(src, out, a, p, n_cubes, st, pca, planar, false);
+    default: return fail(CV_ERR_ARG, "cv_quantize: unknown dtype %d", dtype);
+  }
+}
+
+int cv_dequantize(const void *q, int32_t qdtype, int64_t n_cubes, int64_t T, int64_t HW, int32_t E,
+                  int32_t in_layout, const double *mins, const double *maxs, int32_t bit_depth,
+                  void *out, int32_t out_dtype, uint32_t *err_word, void *stream) {
+  if (!q || !out || !mins || !maxs) return fail(CV_ERR_ARG, "cv_dequantize: null pointer");
+  if (!valid_depth(bit_depth)) return fail(CV_ERR_ARG, "bit depth %d not in (8, 10, 12, 16)", bit_depth);
+  if (E <= 0 || n_cubes < 0 || T < 0 || HW < 0) return fail(CV_ERR_SHAPE, "cv_dequantize: bad sizes");
+  const int64_t n = n_cubes * T * HW * E;
+  if (n == 0) return CV_OK;
+  const int G = (E + 2) / 3;
+  const bool planar = in_layout == CV_LAYOUT_PLANAR;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int NT = 256;
+  int64_t nb = (n + NT - 1) / NT;
+  if (nb > 148 * 64) nb = 148 * 64;
+#define CV_DQ(TQ, TO, PL)                                                                          \
+  k_dequantize<TQ, TO, PL><<<(unsigned)nb, NT, 0, st>>>((const TQ *)q, (TO *)out, n, T, HW, E, G, \
+                                                        mins, maxs, bit_depth, n_cubes, err_word)
+  if (qdtype != CV_U8 && qdtype != CV_U16) return fail(CV_ERR_ARG, "cv_dequantize: q must be u8/u16");
+  if (out_dtype != CV_F32 && out_dtype != CV_F64) return fail(CV_ERR_ARG, "cv_dequantize: out must be f32/f64");
+  if (qdtype == CV_U8) {
+    if (out_dtype == CV_F32) { if (planar) CV_DQ(uint8_t, float, true); else CV_DQ(uint8_t, float, false); }
+    else { if (planar) CV_DQ(uint8_t, double, true); else CV_DQ(uint8_t, double, false); }
+  } else {
+    if (out_dtype == CV_F32) { if (planar) CV_DQ(uint16_t, float, true); else CV_DQ(uint16_t, float, false); }
+    else { if (planar) CV_DQ(uint16_t, double, true); else CV_DQ(uint16_t, double, false); }
+  }
+#undef CV_DQ
+  return check_launch("cv_dequantize");
+}
+
+}  // extern "C"

@@ -1,0 +1,258 @@
+// K1 — per-band statistics with the forward-fill policy, and forward_fill_time.
+//
+// Replaces, for the array path:
+//   fit_quant            /root/reference/pkg/src/cubevid/transform.py:61-70
+//   forward_fill_time    /root/reference/pkg/src/cubevid/cube.py:213-246
+//
+// Work decomposition ("column chunk x time segment"): a CTA owns a contiguous
+// chunk of NT*K elements of the inner (H*W*C) row and a segment of seg_len
+// time steps; every thread owns K elements (tid + k*NT) and walks t inside the
+// segment, so each time step is one fully coalesced sweep of the chunk and the
+// per-element forward-fill carry lives in registers. NT is a multiple of C, so
+// a thread's band is tid % C for all its elements.
+#include "common.cuh"
+
+namespace cvb {
+
+constexpr int kStatsK = 4;
+
+template <typename T> struct AccT { using type = float; };
+template <> struct AccT<double> { using type = double; };
+
+__global__ void k_stats_reset(StatsEntry *ws, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    ws[i].min_key = ~0ull;
+    ws[i].max_key = 0ull;
+    ws[i].nan_count = 0ull;
+    ws[i].lead = 0u;
+    ws[i].pad = 0u;
+  }
+}
+
+template <typename TIn, int K>
+__global__ void __launch_bounds__(1024)
+k_stats(const TIn *__restrict__ src, int64_t T, int64_t inner, int C, int fill_mode, int seg_len,
+        StatsEntry *__restrict__ ws, float *__restrict__ seg_last, uint32_t *err) {
+  using Acc = typename AccT<TIn>::type;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t a = blockIdx.z;
+  const int64_t seg = blockIdx.y;
+  const int64_t nseg = gridDim.y;
+  const int64_t e0 = (int64_t)blockIdx.x * NT * K + tid;
+  const int64_t t0 = seg * seg_len;
+  const int64_t t1 = min(T, t0 + (int64_t)seg_len);
+  const TIn *cube = src + a * T * inner;
+
+  Acc mn = (Acc)INFINITY, mx = (Acc)-INFINITY;
+  unsigned nanc = 0;
+  bool lead = false, inf_seen = false;
+  float last[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) last[k] = __int_as_float(0x7fc00000);
+
+  for (int64_t t = t0; t < t1; ++t) {
+    const TIn *row = cube + t * inner;
+    TIn v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t e = e0 + (int64_t)k * NT;
+      v[k] = (e < inner) ? ldg(row + e) : TIn(0);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t e = e0 + (int64_t)k * NT;
+      if (e >= inner) continue;
+      if constexpr (is_float_t<TIn>::value) {
+        const TIn x = v[k];
+        if (isnan(x)) {
+          ++nanc;
+          if (t == 0) lead = true;
+        } else if (isinf(x)) {
+          inf_seen = true;
+        } else {
+          mn = min(mn, (Acc)x);
+          mx = max(mx, (Acc)x);
+          last[k] = (float)x;
+        }
+      } else {
+        mn = min(mn, (Acc)v[k]);
+        mx = max(mx, (Acc)v[k]);
+      }
+    }
+  }
+  if (seg_last) {
+    float *sl = seg_last + (a * nseg + seg) * inner;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t e = e0 + (int64_t)k * NT;
+      if (e < inner) sl[e] = last[k];
+    }
+  }
+  flag_warp(err, inf_seen, CV_FLAG_NONFINITE);
+  flag_warp(err, fill_mode == 0 && nanc > 0, CV_FLAG_NAN);
+
+  commit_band_stats<Acc>(mn, mx, nanc, lead, C, ws + a * C, smem);
+}
+
+__global__ void k_stats_finalize(const StatsEntry *__restrict__ ws, int64_t n, int fill_mode,
+                                 float fill, double *mins, double *maxs, int64_t *nan_counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const StatsEntry e = ws[i];
+  double mn = INFINITY, mx = -INFINITY;
+  if (e.max_key != 0ull) {
+    mn = dkey_inv(e.min_key);
+    mx = dkey_inv(e.max_key);
+  }
+  if (fill_mode && e.lead) {
+    mn = fmin(mn, (double)fill);
+    mx = fmax(mx, (double)fill);
+  }
+  if (mins) mins[i] = mn;
+  if (maxs) maxs[i] = mx;
+  if (nan_counts) nan_counts[i] = (int64_t)e.nan_count;
+}
+
+// forward_fill_time body: filled values + validity mask, carries in registers.
+template <int K>
+__global__ void __launch_bounds__(256)
+k_forward_fill(const float *__restrict__ src, int64_t T, int64_t inner, float fill, int seg_len,
+               const float *__restrict__ seg_last, float *__restrict__ out,
+               uint8_t *__restrict__ mask, uint32_t *err) {
+  const int NT = blockDim.x;
+  const int64_t a = blockIdx.z;
+  const int64_t seg = blockIdx.y;
+  const int64_t nseg = gridDim.y;
+  const int64_t e0 = (int64_t)blockIdx.x * NT * K + threadIdx.x;
+  const int64_t t0 = seg * seg_len;
+  const int64_t t1 = min(T, t0 + (int64_t)seg_len);
+  const float *cube = src + a * T * inner;
+  const float *sl = seg_last + a * nseg * inner;
+  float carry[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int64_t e = e0 + (int64_t)k * NT;
+    carry[k] = fill;
+    if (e < inner) {
+      for (int64_t s = seg - 1; s >= 0; --s) {
+        float v = sl[s * inner + e];
+        if (!isnan(v)) {
+          carry[k] = v;
+          break;
+        }
+      }
+    }
+  }
+  bool inf_seen = false;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t off = (a * T + t) * inner;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t e = e0 + (int64_t)k * NT;
+      if (e >= inner) continue;
+      float v = __ldg(cube + t * inner + e);
+      const bool ok = !isnan(v);
+      if (ok) {
+        inf_seen |= isinf(v);
+        carry[k] = v;
+      }
+      out[off + e] = carry[k];
+      mask[off + e] = ok ? 1 : 0;
+    }
+  }
+  flag_warp(err, inf_seen, CV_FLAG_NONFINITE);
+}
+
+template <typename TIn>
+static void launch_stats(const void *src, int64_t n, int64_t T, int64_t inner, int C,
+                         int fill_mode, int seg_len, void *ws, float *seg_last, uint32_t *err,
+                         cudaStream_t st) {
+  using Acc = typename AccT<TIn>::type;
+  const int NT = threads_for_channels(C);
+  const int64_t nchunk = (inner + (int64_t)NT * kStatsK - 1) / ((int64_t)NT * kStatsK);
+  const int64_t nseg = (T + seg_len - 1) / seg_len;
+  dim3 grid((unsigned)nchunk, (unsigned)nseg, (unsigned)n);
+  size_t sm = (size_t)NT * (2 * sizeof(Acc) + 2 * sizeof(unsigned));
+  k_stats<TIn, kStatsK><<<grid, NT, sm, st>>>((const TIn *)src, T, inner, C, fill_mode, seg_len,
+                                               (StatsEntry *)ws, seg_last, err);
+}
+
+}  // namespace cvb
+
+using namespace cvb;
+
+extern "C" {
+
+size_t cv_stats_ws_bytes(int64_t n_cubes, int32_t C) {
+  return (size_t)(n_cubes * C) * sizeof(StatsEntry);
+}
+
+int64_t cv_num_segments(int64_t T, int32_t seg_len) {
+  if (seg_len <= 0) return -1;
+  return (T + seg_len - 1) / seg_len;
+}
+
+int cv_stats_reset(void *stats_ws, int64_t n_cubes, int32_t C, void *stream) {
+  if (!stats_ws || n_cubes < 0 || C <= 0) return fail(CV_ERR_ARG, "cv_stats_reset: bad arguments");
+  const int64_t n = n_cubes * C;
+  if (n == 0) return CV_OK;
+  k_stats_reset<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (StatsEntry *)stats_ws, n);
+  return check_launch("cv_stats_reset");
+}
+
+int cv_stats(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int64_t inner, int32_t C,
+             int32_t fill_mode, int32_t seg_len, void *stats_ws, float *seg_last,
+             uint32_t *err_word, void *stream) {
+  if (!src || !stats_ws) return fail(CV_ERR_ARG, "cv_stats: null pointer");
+  if (C <= 0 || C > kMaxC)
+    return fail(CV_ERR_UNSUPPORTED, "cv_stats: %d channels (supported 1..%d)", C, kMaxC);
+  if (n_cubes < 0 || T < 0 || inner < 0 || inner % C != 0)
+    return fail(CV_ERR_SHAPE, "cv_stats: inner=%lld is not a multiple of C=%d", (long long)inner, C);
+  if (seg_len <= 0) return fail(CV_ERR_ARG, "cv_stats: seg_len must be positive");
+  if (n_cubes > 65535 || cv_num_segments(T, seg_len) > 65535)
+    return fail(CV_ERR_UNSUPPORTED, "cv_stats: grid too large (n_cubes or T/seg_len > 65535)");
+  if (n_cubes == 0 || T == 0 || inner == 0) return CV_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (dtype) {
+    case CV_F32: launch_stats<float>(src, n_cubes, T, inner, C, fill_mode, seg_len, stats_ws, seg_last, err_word, st); break;
+    case CV_F64: launch_stats<double>(src, n_cubes, T, inner, C, fill_mode, seg_len, stats_ws, nullptr, err_word, st); break;
+    case CV_U16: launch_stats<uint16_t>(src, n_cubes, T, inner, C, 0, seg_len, stats_ws, nullptr, err_word, st); break;
+    case CV_U8: launch_stats<uint8_t>(src, n_cubes, T, inner, C, 0, seg_len, stats_ws, nullptr, err_word, st); break;
+    default: return fail(CV_ERR_ARG, "cv_stats: unknown dtype %d", dtype);
+  }
+  return check_launch("cv_stats");
+}
+
+int cv_stats_finalize(const void *stats_ws, int64_t n_cubes, int32_t C, int32_t fill_mode,
+                      float fill_value, double *mins, double *maxs, int64_t *nan_counts,
+                      void *stream) {
+  if (!stats_ws || C <= 0 || n_cubes < 0) return fail(CV_ERR_ARG, "cv_stats_finalize: bad arguments");
+  const int64_t n = n_cubes * C;
+  if (n == 0) return CV_OK;
+  k_stats_finalize<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const StatsEntry *)stats_ws, n, fill_mode, fill_value, mins, maxs, nan_counts);
+  return check_launch("cv_stats_finalize");
+}
+
+int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner, float fill_value,
+                    int32_t seg_len, const float *seg_last, float *out, uint8_t *mask,
+                    uint32_t *err_word, void *stream) {
+  if (!src || !out || !mask || !seg_last) return fail(CV_ERR_ARG, "cv_forward_fill: null pointer");
+  if (n_outer < 0 || T < 0 || inner < 0 || seg_len <= 0) return fail(CV_ERR_SHAPE, "cv_forward_fill: bad sizes");
+  if (n_outer > 65535 || cv_num_segments(T, seg_len) > 65535)
+    return fail(CV_ERR_UNSUPPORTED, "cv_forward_fill: grid too large");
+  if (n_outer == 0 || T == 0 || inner == 0) return CV_OK;
+  constexpr int K = 4;
+  const int NT = 256;
+  dim3 grid((unsigned)((inner + NT * K - 1) / (NT * K)), (unsigned)cv_num_segments(T, seg_len),
+            (unsigned)n_outer);
+  k_forward_fill<K><<<grid, NT, 0, (cudaStream_t)stream>>>(src, T, inner, fill_value, seg_len,
+                                                            seg_last, out, mask, err_word);
+  return check_launch("cv_forward_fill");
+}
+
+}  // extern "C"

@@ -1,0 +1,306 @@
+"""GPU parity: every sm_100a entry point against the reference's golden vectors
+and the CPU oracle. Integer outputs bit-exact; floats within the stated
+tolerances (PSNR 0.01 dB, SSIM 1e-5 per band, PCA basis up to 1e-9 in |cos|)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cubevid_oracle as O
+from oracle import metrics_oracle as M
+from paper_2506_19656_b200 import ConfigurationError
+from paper_2506_19656_b200 import cube as G_cube
+from paper_2506_19656_b200 import metrics as G_metrics
+from paper_2506_19656_b200 import pipeline as G_pipe
+from paper_2506_19656_b200 import transform as G
+
+pytestmark = pytest.mark.gpu
+
+PSNR_TOL_DB = 0.01
+SSIM_TOL = 1e-5
+
+
+# ------------------------------------------------------------------ forward fill
+
+@pytest.mark.parametrize("name,fv", [("t0_f0", 0.0), ("t0_f01", 0.1), ("t0_fm3", -3.5)])
+def test_forward_fill_golden(cuda, golden, name, fv):
+    f, m = G_cube.forward_fill_time(golden["fill_in"], 0, fv)
+    np.testing.assert_array_equal(f.view(np.uint32), golden[f"fill_{name}_out"].view(np.uint32))
+    np.testing.assert_array_equal(m.mask, golden[f"fill_{name}_mask"])
+
+
+def test_forward_fill_axes_ints_errors(cuda, golden, golden_errors):
+    f, m = G_cube.forward_fill_time(golden["fill_ax2_in"], 2, 0.0)
+    np.testing.assert_array_equal(f, golden["fill_ax2_out"])
+    np.testing.assert_array_equal(m.mask, golden["fill_ax2_mask"])
+    f, m = G_cube.forward_fill_time(golden["fill_ax2_in"], -2, 0.25)
+    np.testing.assert_array_equal(f, golden["fill_axm2_out"])
+    f, m = G_cube.forward_fill_time(golden["fill_int_in"], 0)
+    np.testing.assert_array_equal(f, golden["fill_int_out"])
+    assert m.all_observed
+    bad = golden["fill_in"].copy()
+    bad[1, 1, 1, 1] = np.inf
+    with pytest.raises(ConfigurationError) as e:
+        G_cube.forward_fill_time(bad, 0)
+    assert str(e.value) == golden_errors["fill_inf"]
+    with pytest.raises(ConfigurationError) as e:
+        G_cube.forward_fill_time(golden["fill_in"], 4)
+    assert str(e.value) == golden_errors["fill_axis"]
+
+
+@pytest.mark.parametrize("shape,axis", [((70, 9, 11, 3), 0), ((5, 300, 7), 1), ((1, 4, 4, 2), 0),
+                                        ((200, 3), 0)])
+def test_forward_fill_long_runs_vs_oracle(cuda, shape, axis):
+    rng = np.random.default_rng(7)
+    x = rng.random(shape).astype(np.float32)
+    x[rng.random(shape) < 0.6] = np.nan   # long gaps: exercises the segment carries
+    f, m = G_cube.forward_fill_time(x, axis, 0.5)
+    fo, mo = O.forward_fill(x, axis, 0.5)
+    np.testing.assert_array_equal(f, fo)
+    np.testing.assert_array_equal(m.mask, mo)
+    assert m.n_synthesized == int((~mo).sum())
+
+
+def test_forward_fill_device_tensor(cuda):
+    x = torch.rand((40, 8, 8, 2), device=cuda)
+    x[5:30] = float("nan")
+    f, m = G_cube.forward_fill_time(x, 0)
+    assert f.is_cuda
+    fo, _ = O.forward_fill(x.cpu().numpy(), 0)
+    np.testing.assert_array_equal(f.cpu().numpy(), fo)
+
+
+# ------------------------------------------------------------------ quantisation
+
+@pytest.mark.parametrize("B", [8, 10, 12, 16])
+def test_fit_quant_quantize_dequantize_golden(cuda, golden, B):
+    x = golden["q_in"]
+    p = G.fit_quant(x, B)
+    np.testing.assert_array_equal(np.array(p.mins), golden[f"q{B}_mins"])
+    np.testing.assert_array_equal(np.array(p.maxs), golden[f"q{B}_maxs"])
+    q = G.quantize(x, p)
+    assert q.dtype == golden[f"q{B}_out"].dtype
+    np.testing.assert_array_equal(q, golden[f"q{B}_out"])
+    dq = G.dequantize(q, p)
+    assert dq.dtype == np.float64
+    np.testing.assert_array_equal(dq.view(np.uint64), golden[f"dq{B}_out"].view(np.uint64))
+
+
+@pytest.mark.parametrize("B", [8, 10, 12, 16])
+def test_quantize_ties_constant(cuda, golden, B):
+    x = golden["ties_in"]
+    p = G.fit_quant(x, B)
+    np.testing.assert_array_equal(G.quantize(x, p), golden[f"ties{B}_out"])
+
+
+def test_quantize_clamp_u16_f64_errors(cuda, golden, golden_errors):
+    pc = G.QuantParams(12, (0.2, 0.0, 0.0), (0.8, 1.0, 1.0))
+    np.testing.assert_array_equal(G.quantize(golden["q_in"], pc, clamp=True), golden["clamp12_out"])
+    with pytest.raises(ConfigurationError) as e:
+        G.quantize(golden["q_in"], pc)
+    assert str(e.value) == golden_errors["quantize_range"]
+    with pytest.raises(ConfigurationError) as e:
+        G.fit_quant(golden["fill_in"], 8)
+    assert str(e.value) == golden_errors["fit_nonfinite"]
+    p = G.fit_quant(golden["u16_in"], 8)
+    np.testing.assert_array_equal(np.array(p.mins), golden["u16_mins"])
+    np.testing.assert_array_equal(G.quantize(golden["u16_in"], p), golden["u16_q8"])
+    p = G.fit_quant(golden["f64_in"], 16)
+    np.testing.assert_array_equal(np.array(p.maxs), golden["f64_maxs"])
+    np.testing.assert_array_equal(G.quantize(golden["f64_in"], p), golden["f64_q16"])
+    with pytest.raises(ConfigurationError) as e:
+        G.dequantize(np.full((1, 1, 1, 3), 300, np.uint16), G.QuantParams(8, (0,) * 3, (1,) * 3))
+    assert str(e.value) == golden_errors["dequant_range"]
+
+
+@pytest.mark.parametrize("B", [8, 10, 12, 16])
+def test_quantize_random_vs_oracle(cuda, B):
+    """10^6 samples per depth (SPEC acceptance test 2 uses 10^6 at B=12/16)."""
+    rng = np.random.default_rng(B)
+    x = (rng.random((10, 100, 100, 10)) * rng.choice([1.0, 1e-3, 1e4], 10) +
+         rng.normal(size=10) * 100).astype(np.float32)
+    lo, hi = O.fit_quant(x)
+    q = G.quantize(x, G.QuantParams(B, tuple(lo), tuple(hi)))
+    np.testing.assert_array_equal(q, O.quantize(x, lo, hi, B))
+    dq = G.dequantize(q, G.QuantParams(B, tuple(lo), tuple(hi)))
+    np.testing.assert_array_equal(dq, O.dequantize(q, lo, hi, B))
+    step = (hi - lo) / O.LEVELS[B]
+    assert (np.abs(dq - x) <= step / 2 * (1 + 1e-12) + 1e-300).all()
+
+
+def test_quantize_exhaustive_8bit(cuda):
+    """Every 8-bit level and every half-way point between levels (ties)."""
+    L = 255
+    v = np.arange(0, 2 * L + 1, dtype=np.float64) / (2 * L)
+    x = np.stack([v, v * 3 - 1, v * 1e-6 + 2], axis=-1).reshape(1, 1, -1, 3)
+    lo, hi = O.fit_quant(x)
+    np.testing.assert_array_equal(G.quantize(x, G.QuantParams(8, tuple(lo), tuple(hi))),
+                                  O.quantize(x, lo, hi, 8))
+
+
+def test_quantize_nan_and_empty(cuda):
+    x = np.zeros((2, 3, 3, 2), np.float32)
+    x[0, 0, 0, 0] = np.nan
+    with pytest.raises(ConfigurationError):
+        G.quantize(x, G.QuantParams(8, (0.0, 0.0), (1.0, 1.0)))
+    e = G.quantize(np.zeros((0, 3, 3, 2), np.float32), G.QuantParams(8, (0.0, 0.0), (1.0, 1.0)))
+    assert e.shape == (0, 3, 3, 2) and e.dtype == np.uint8
+    with pytest.raises(ValueError):
+        G.fit_quant(np.zeros((0, 3, 3, 2), np.float32), 8)
+    with pytest.raises(ConfigurationError):
+        G.fit_quant(np.zeros((3, 3, 2), np.float32), 8)
+
+
+# ------------------------------------------------------------------ PCA
+
+def _cos_match(a, b, tol):
+    cos = np.abs((a * b).sum(axis=1)) / (np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1))
+    assert (cos >= 1 - tol).all(), cos
+
+
+def test_pca_golden(cuda, golden, golden_errors):
+    x = golden["pca_in"]
+    m = G.pca_fit(x, 3)
+    np.testing.assert_allclose(m.mean, golden["pca_mean"], rtol=1e-12)
+    _cos_match(m.components, golden["pca_comps"], 1e-9)
+    np.testing.assert_allclose(m.components, golden["pca_comps"], atol=1e-8)  # same sign rule
+    np.testing.assert_allclose(m.explained_variance, golden["pca_ev"], rtol=1e-9)
+    pcs = G.pca_forward(x, m)
+    np.testing.assert_allclose(pcs, golden["pca_fwd"], atol=1e-7)
+    np.testing.assert_allclose(G.pca_inverse(pcs, m), golden["pca_inv"], atol=1e-7)
+    full = G.pca_fit(x, 5)
+    back = G.pca_inverse(G.pca_forward(x, full), full)
+    np.testing.assert_allclose(back, x, atol=1e-6 * (x.max() - x.min()))
+    np.testing.assert_allclose(full.explained_variance.sum(),
+                               x.reshape(-1, 5).astype(np.float64).var(axis=0).sum(), rtol=1e-8)
+    with pytest.raises(ConfigurationError) as e:
+        G.pca_fit(x, 6)
+    assert str(e.value) == golden_errors["pca_nkeep"]
+
+
+def test_pca_rank1_and_mean_only(cuda):
+    rng = np.random.default_rng(3)
+    r = rng.normal(size=(3, 4, 5, 1))
+    m = G.pca_fit(np.concatenate([r, 2 * r], axis=-1), 1)
+    frac = m.explained_variance[0] / np.var(np.concatenate([r, 2 * r], -1).reshape(-1, 2), axis=0).sum()
+    assert abs(frac - 1.0) < 1e-9
+    const = np.ones((2, 3, 3, 4)) * np.array([1.0, 2.0, 3.0, 4.0])
+    const[0, 0, 0] += 1e-3
+    mc = G.pca_fit(const, 2)
+    pcs = G.pca_forward(np.ones((1, 2, 2, 4)) * mc.mean, mc)
+    assert np.abs(pcs).max() < 1e-12
+
+
+# ------------------------------------------------------------------ metrics
+
+@pytest.mark.parametrize("seed", range(5))
+def test_metrics_vs_oracle(cuda, seed):
+    rng = np.random.default_rng(seed)
+    o = rng.random((3, 20, 24, 3)) + 0.1
+    r = o + 0.02 * rng.normal(size=o.shape)
+    db, agg = G_metrics.psnr(o, r)
+    dbo, aggo = M.psnr(o, r)
+    np.testing.assert_allclose(db, dbo, rtol=1e-12)
+    np.testing.assert_allclose(G_metrics.ssim_per_band(o.astype(np.float32), r),
+                               M.ssim_per_band(o.astype(np.float32), r), atol=SSIM_TOL)
+    assert abs(G_metrics.ssim(o, o) - 1.0) < 1e-6
+
+
+def test_metrics_known_answers(cuda):
+    o = np.array([0, 1, 2, 3], dtype=np.float64).reshape(1, 1, 4, 1)
+    r = np.array([0, 1, 2, 2], dtype=np.float64).reshape(1, 1, 4, 1)
+    db, agg = G_metrics.psnr(o, r)
+    assert abs(agg - 15.563025007672874) < 1e-9
+    with pytest.raises(ConfigurationError):
+        G_metrics.ssim(np.zeros((1, 8, 8, 1)), np.zeros((1, 8, 8, 1)))
+    yy, xx = np.mgrid[0:16, 0:16]
+    pat = (((yy // 2) + (xx // 2)) % 2 * 2 - 1).astype(np.float64)
+    assert G_metrics.ssim((1.0 + 0.5 * pat)[None, :, :, None], (1.0 - 0.5 * pat)[None, :, :, None]) < 0
+
+
+# ------------------------------------------------------------------ fused stream
+
+@pytest.mark.parametrize("seg_len", [16, 3, 1])
+def test_stream_golden(cuda, golden, seg_len):
+    x = golden["stream_in"]
+    spec = G_pipe.StreamSpec(10, seg_len=seg_len)
+    enc, recon, sc = G_pipe.roundtrip(torch.from_numpy(x).to(cuda), spec)
+    enc.check()
+    np.testing.assert_array_equal(enc.qmins[0].cpu().numpy(), golden["stream_mins"])
+    np.testing.assert_array_equal(enc.qmaxs[0].cpu().numpy(), golden["stream_maxs"])
+    np.testing.assert_array_equal(enc.frames[0].cpu().numpy(), golden["stream_frames"])
+    np.testing.assert_array_equal(recon.cpu().numpy(), golden["stream_recon"].astype(np.float32))
+    rep = sc.report()[0]
+    dbo, aggo = M.psnr(golden["stream_filled"], golden["stream_recon"])
+    np.testing.assert_allclose(rep["psnr_per_band"], dbo, rtol=1e-9)
+    so = M.ssim_per_band(golden["stream_filled"], golden["stream_recon"])
+    np.testing.assert_allclose(rep["ssim_per_band"], so, atol=SSIM_TOL)
+    assert int(enc.nan_counts.sum()) == int(np.isnan(x).sum())
+
+
+def test_stream_zero_pad_and_noisy_frames(cuda, golden):
+    x = golden["stream_in"]
+    spec = G_pipe.StreamSpec(10, pad_mode="zero")
+    enc = G_pipe.encode_prep(torch.from_numpy(x).to(cuda), spec)
+    ref = O.encode_stream(x, 10, pad_zero=True)
+    np.testing.assert_array_equal(enc.frames[0].cpu().numpy(), ref["frames"])
+    noisy = O.decoded_frames_with_noise(ref["frames"], 10)
+    recon, sc = G_pipe.decode_eval(enc, torch.from_numpy(x).to(cuda),
+                                   frames=torch.from_numpy(noisy[None]).to(cuda))
+    rec_o = O.decode_stream(noisy, ref, x.shape, 10)
+    np.testing.assert_array_equal(recon.cpu().numpy(), rec_o.astype(np.float32))
+    rep = sc.report()[0]
+    np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), rtol=1e-9)
+    np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
+
+
+@pytest.mark.parametrize("shape,C_pcs,B", [((6, 13, 17, 1), 0, 8), ((4, 12, 12, 32), 0, 12),
+                                           ((3, 15, 19, 5), 0, 16), ((2, 21, 11, 12), 9, 12),
+                                           ((5, 11, 30, 4), 2, 16)])
+def test_stream_edge_shapes(cuda, shape, C_pcs, B):
+    rng = np.random.default_rng(11)
+    x = (rng.random(shape) * 3 - 1).astype(np.float32)
+    if C_pcs == 0:
+        x[rng.random(shape) < 0.1] = np.nan
+    enc, recon, sc = G_pipe.roundtrip(torch.from_numpy(x).to(cuda), G_pipe.StreamSpec(B, n_pcs=C_pcs))
+    enc.check()
+    ref = O.encode_stream(x, B, n_pcs=C_pcs)
+    if C_pcs == 0:
+        np.testing.assert_array_equal(enc.frames[0].cpu().numpy(), ref["frames"])
+        rec_o = O.decode_stream(ref["frames"], ref, x.shape, B)
+        np.testing.assert_array_equal(recon.cpu().numpy(), rec_o.astype(np.float32))
+    else:
+        got = enc.frames[0].cpu().numpy().astype(np.int64)
+        diff = np.abs(got - ref["frames"].astype(np.int64))
+        assert diff.max() <= 1 and (diff > 0).mean() <= 0.02
+        rec_o = O.decode_stream(ref["frames"], ref, x.shape, B)
+    rep = sc.report()[0]
+    np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o),
+                               atol=PSNR_TOL_DB)
+    np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
+
+
+def test_all_nan_and_constant_bands(cuda):
+    x = np.random.default_rng(1).random((8, 12, 12, 3)).astype(np.float32)
+    x[..., 1] = np.nan          # never observed -> fill constant everywhere -> constant band
+    x[..., 2] = 0.25            # constant
+    x[:2, ..., 0] = np.nan      # leading gap -> fill enters the range
+    enc, recon, sc = G_pipe.roundtrip(torch.from_numpy(x).to(cuda), G_pipe.StreamSpec(8, fill_value=0.5))
+    ref = O.encode_stream(x, 8, fill=0.5)
+    np.testing.assert_array_equal(enc.qmins[0].cpu().numpy(), ref["mins"])
+    np.testing.assert_array_equal(enc.frames[0].cpu().numpy(), ref["frames"])
+    rep = sc.report()[0]
+    assert np.isinf(rep["psnr_per_band"][1]) and np.isinf(rep["psnr_per_band"][2])
+
+
+def test_batch_matches_single(cuda):
+    from paper_2506_19656_b200 import synth
+
+    cubes = synth.minicube_batch(3, 100, (12, 16, 20, 7), device=cuda)
+    spec = G_pipe.StreamSpec(10, seg_len=4)
+    encb, reconb, scb = G_pipe.roundtrip(cubes, spec)
+    for b in range(3):
+        enc1, recon1, sc1 = G_pipe.roundtrip(cubes[b].contiguous(), spec)
+        assert torch.equal(encb.frames[b], enc1.frames[0])
+        assert torch.equal(reconb[b], recon1)
+        np.testing.assert_array_equal(scb.report()[b]["psnr_per_band"], sc1.report()[0]["psnr_per_band"])
