@@ -136,7 +136,9 @@ int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner,
  * pointers (the model comes from the host eigh); they are passed to the
  * kernel by value and shared by all n_cubes.
  * mins/maxs: [n_cubes][E] float64.
- * fill_mode 1 forward-fills NaN along T using seg_last (see cv_stats).
+ * fill_mode 1 forward-fills NaN along T using seg_last (see cv_stats);
+ * filled_out (nullable, f32 input only) then receives the filled cube, i.e.
+ * forward_fill_time's output (cube.py:244-246), in the same pass.
  * out_layout CHANNEL_LAST: out [n_cubes][T][HW][E] (what quantize returns).
  * out_layout PLANAR: out [n_cubes][G][T][3][HW], planes padded per pad_mode
  *   (plan.py:118-128 + bridge.py:157-160).
@@ -148,7 +150,7 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T,
                 float fill_value, int32_t seg_len, const float *seg_last,
                 const double *pca_mean, const double *pca_comps, int32_t n_pcs,
                 int32_t out_layout, int32_t pad_mode, void *out,
-                uint32_t *err_word, void *stream);
+                float *filled_out, uint32_t *err_word, void *stream);
 
 /*
  * dequantize (transform.py:108-126), bit-exact in float64:
@@ -219,8 +221,9 @@ size_t cv_eval_ws_bytes(int64_t n_cubes, int64_t T, int64_t H, int64_t W,
  *            inv_comps[j][c] + inv_mean[c] (HOST pointers [E][C], [C],
  *            shared by all cubes, passed by value);
  *   recon_in channel-last [n][T][HW][C] (rdtype f32/f64).
- * Original: orig [n][T][HW][C] (odtype), forward-filled per fill_mode /
- * seg_last exactly as cv_quantize does (the codec saw the filled cube).
+ * Original: orig [n][T][HW][C] (odtype f32/f64/u16), already forward-filled
+ * (the codec saw the filled cube): pass cv_quantize's
+ * filled_out or cv_forward_fill's output. NaN sets CV_FLAG_NAN.
  * Outputs: recon_out (nullable) channel-last f32; sse [n][C] = sum of squared
  * error in float64; when want_ssim, ssim_sum [n][C] = sum over the valid
  * (H-10)x(W-10) region of every frame of the 11x11 Gaussian (sigma 1.5)
@@ -229,11 +232,10 @@ size_t cv_eval_ws_bytes(int64_t n_cubes, int64_t T, int64_t H, int64_t W,
 int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins,
             const double *qmaxs, int32_t bit_depth, const double *inv_mean,
             const double *inv_comps, const void *recon_in, int32_t rdtype,
-            const void *orig, int32_t odtype, int32_t fill_mode,
-            float fill_value, int32_t seg_len, const float *seg_last,
-            int64_t n_cubes, int64_t T, int64_t H, int64_t W, int32_t C,
-            const double *peaks, int32_t want_ssim, float *recon_out, void *ws,
-            double *sse, double *ssim_sum, uint32_t *err_word, void *stream);
+            const void *orig, int32_t odtype, int64_t n_cubes, int64_t T,
+            int64_t H, int64_t W, int32_t C, const double *peaks,
+            int32_t want_ssim, float *recon_out, void *ws, double *sse,
+            double *ssim_sum, uint32_t *err_word, void *stream);
 
 #ifdef __cplusplus
 }

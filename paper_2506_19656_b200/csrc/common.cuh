@@ -178,11 +178,26 @@ __device__ __forceinline__ uint32_t quantize_value(double v, const QBand &b) {
   return (uint32_t)q;
 }
 
-// dequantize (transform.py:122-125): min + (q / L) * (max - min)
+// RN(q / L) without a division: q0 = RN(q*rL), e = fma(-q0, L, q) (exact),
+// RN(q0 + e*rL). Equal to the IEEE quotient for every q in [0, L] at all four
+// bit depths (exhaustive proof: tests/test_exactness.py).
+__device__ __forceinline__ double div_by_levels(double q, double L, double rL) {
+  const double q0 = __dmul_rn(q, rL);
+  const double e = __fma_rn(-q0, L, q);
+  return __fma_rn(e, rL, q0);
+}
+
+// dequantize (transform.py:122-125): min + (q / L) * (max - min), same rounding
+// as numpy's float64 evaluation order.
 __device__ __forceinline__ double dequantize_value(uint32_t q, double m, double span, double L,
                                                    bool constant) {
   if (constant) return m;
-  return __dadd_rn(m, __dmul_rn(__ddiv_rn((double)q, L), span));
+  return __dadd_rn(m, __dmul_rn(div_by_levels((double)q, L, __drcp_rn(L)), span));
+}
+
+__device__ __forceinline__ double dequantize_fast(uint32_t q, double m, double span, double L,
+                                                  double rL) {
+  return __dadd_rn(m, __dmul_rn(div_by_levels((double)q, L, rL), span));
 }
 
 }  // namespace cvb

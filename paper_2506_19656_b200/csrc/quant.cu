@@ -45,6 +45,7 @@ struct QuantArgs {
   int seg_len;
   const double *mins, *maxs;
   const float *seg_last;
+  float *filled_out;
   uint32_t *err;
 };
 
@@ -134,6 +135,8 @@ k_quantize(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs 
       for (int k = 0; k < kQK; ++k) {
         if (isnan(v[k])) v[k] = (S)carry[k];
         else carry[k] = (float)v[k];
+        const int64_t e = e0 + (int64_t)k * NT;
+        if (args.filled_out && e < inner) args.filled_out[(a * T + t) * inner + e] = (float)v[k];
       }
     }
     if constexpr (!PCA) {
@@ -214,6 +217,183 @@ k_quantize(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs 
   }
   flag_warp(args.err, bad, CV_FLAG_RANGE);
   flag_warp(args.err, nanbad, CV_FLAG_NAN);
+}
+
+// Vectorised non-PCA quantiser for rows whose length is a multiple of 4:
+// each thread loads KV vectors of 4 consecutive elements per time step
+// (16 B for f32, 8 B for u16) and keeps the next step's vectors in flight
+// while the current one is quantised. NT is a multiple of C, so the band of
+// vector lane j is fixed per thread: (4*tid + j) % C.
+template <typename TIn> struct Vec4T;
+template <> struct Vec4T<float> { using type = float4; };
+template <> struct Vec4T<uint16_t> { using type = ushort4; };
+template <> struct Vec4T<uint8_t> { using type = uchar4; };
+template <typename TOut> struct OutVec4T;
+template <> struct OutVec4T<uint8_t> { using type = uchar4; };
+template <> struct OutVec4T<uint16_t> { using type = ushort4; };
+
+template <typename TIn, typename TOut, bool PLANAR, bool FILL, int KV>
+__global__ void __launch_bounds__(1024)
+k_quantize_vec(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs args) {
+  using V = typename Vec4T<TIn>::type;
+  using OV = typename OutVec4T<TOut>::type;
+  constexpr int VEC = 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int C = args.C;
+  const int64_t T = args.T, HW = args.HW, inner = HW * C;
+  const int PK = NT * VEC / C;  // pixels per k-step of the chunk
+  const int P = PK * KV;        // pixels per chunk
+  const int64_t a = blockIdx.z, seg = blockIdx.y, nseg = gridDim.y;
+  const int64_t pix0 = (int64_t)blockIdx.x * P;
+  const int64_t e0 = pix0 * C;
+  const int64_t t0 = seg * args.seg_len;
+  const int64_t t1 = min(T, t0 + (int64_t)args.seg_len);
+  const TIn *cube = src + a * T * inner;
+  TOut *sq = reinterpret_cast<TOut *>(smem);  // [2][C][P]
+
+  QBand qb[VEC];
+  int cj[VEC], pj[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const int el = VEC * tid + j;
+    cj[j] = el % C;
+    pj[j] = el / C;
+    qb[j] = make_qband(args.mins[a * C + cj[j]], args.maxs[a * C + cj[j]], args.bit_depth);
+  }
+  int64_t voff[KV];
+  bool vok[KV];
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    voff[k] = e0 + (int64_t)VEC * (tid + k * NT);
+    vok[k] = voff[k] < inner;
+  }
+  float carry[KV][VEC];
+  if constexpr (FILL) {
+    const float *sl = args.seg_last + a * nseg * inner;
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        carry[k][j] = args.fill;
+        if (vok[k]) {
+          for (int64_t s = seg - 1; s >= 0; --s) {
+            const float v = sl[s * inner + voff[k] + j];
+            if (!isnan(v)) {
+              carry[k][j] = v;
+              break;
+            }
+          }
+        }
+      }
+  }
+
+  V cur[KV], nxt[KV];
+#pragma unroll
+  for (int k = 0; k < KV; ++k)
+    if (vok[k]) cur[k] = __ldg(reinterpret_cast<const V *>(cube + t0 * inner + voff[k]));
+  bool bad = false, nanbad = false;
+  const bool full_chunk = (pix0 + P <= HW);
+  int buf = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    if (t + 1 < t1) {
+#pragma unroll
+      for (int k = 0; k < KV; ++k)
+        if (vok[k]) nxt[k] = __ldg(reinterpret_cast<const V *>(cube + (t + 1) * inner + voff[k]));
+    }
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      if (!vok[k]) continue;
+      float x[VEC] = {(float)cur[k].x, (float)cur[k].y, (float)cur[k].z, (float)cur[k].w};
+      if constexpr (FILL) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if (isnan(x[j])) x[j] = carry[k][j];
+          else carry[k][j] = x[j];
+        }
+        if (args.filled_out)
+          *reinterpret_cast<float4 *>(args.filled_out + (a * T + t) * inner + voff[k]) =
+              make_float4(x[0], x[1], x[2], x[3]);
+      }
+      uint32_t q[VEC];
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        if constexpr (!FILL) nanbad |= isnan(x[j]);
+        const double d = range_prep((double)x[j], qb[j], args.clamp, bad);
+        q[j] = quantize_value(d, qb[j]);
+      }
+      if constexpr (PLANAR) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) sq[((size_t)buf * C + cj[j]) * P + pj[j] + k * PK] = (TOut)q[j];
+      } else {
+        OV o;
+        o.x = (TOut)q[0];
+        o.y = (TOut)q[1];
+        o.z = (TOut)q[2];
+        o.w = (TOut)q[3];
+        *reinterpret_cast<OV *>(out + (a * T + t) * inner + voff[k]) = o;
+      }
+    }
+    if constexpr (PLANAR) {
+      __syncthreads();
+      const int nplanes = 3 * args.G;
+      const TOut *sb = sq + (size_t)buf * C * P;
+      constexpr int OVEC = 16 / sizeof(TOut);
+      const bool vec_ok = full_chunk && ((HW * (int64_t)sizeof(TOut)) % 16 == 0) && (P % OVEC == 0);
+      if (vec_ok) {
+        const int nv = P / OVEC;
+        for (int i = tid; i < nplanes * nv; i += NT) {
+          const int pl = i / nv, vi = i % nv;
+          const int g = pl / 3, jp = pl % 3;
+          TOut *dst = out + (((a * args.G + g) * T + t) * 3 + jp) * HW + pix0 + (int64_t)vi * OVEC;
+          uint4 val = make_uint4(0, 0, 0, 0);
+          if (pl < C || args.pad_mode == CV_PAD_REPEAT) {
+            const int sp = pl < C ? pl : C - 1;
+            val = *reinterpret_cast<const uint4 *>(sb + (size_t)sp * P + (size_t)vi * OVEC);
+          }
+          *reinterpret_cast<uint4 *>(dst) = val;
+        }
+      } else {
+        for (int i = tid; i < nplanes * P; i += NT) {
+          const int pl = i / P, p = i % P;
+          if (pix0 + p >= HW) continue;
+          const int g = pl / 3, jp = pl % 3;
+          TOut val = 0;
+          if (pl < C || args.pad_mode == CV_PAD_REPEAT) val = sb[(size_t)(pl < C ? pl : C - 1) * P + p];
+          out[(((a * args.G + g) * T + t) * 3 + jp) * HW + pix0 + p] = val;
+        }
+      }
+      buf ^= 1;
+    }
+#pragma unroll
+    for (int k = 0; k < KV; ++k) cur[k] = nxt[k];
+  }
+  flag_warp(args.err, bad, CV_FLAG_RANGE);
+  flag_warp(args.err, nanbad, CV_FLAG_NAN);
+}
+
+template <typename TIn, typename TOut, bool PLANAR, bool FILL>
+static int launch_qv(const void *src, void *out, const QuantArgs &args, int64_t n_cubes,
+                     cudaStream_t st) {
+  constexpr int KV = 2;
+  const int NT = threads_for_channels(args.C);
+  const int P = NT * 4 * KV / args.C;
+  const size_t sm = PLANAR ? 2 * (size_t)args.C * P * sizeof(TOut) : 0;
+  auto kern = k_quantize_vec<TIn, TOut, PLANAR, FILL, KV>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((unsigned)((args.HW + P - 1) / P), (unsigned)cv_num_segments(args.T, args.seg_len),
+            (unsigned)n_cubes);
+  kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args);
+  return check_launch("cv_quantize(vec)");
+}
+
+template <typename TIn, typename TOut>
+static int dispatch_qv(const void *src, void *out, const QuantArgs &a, int64_t n, cudaStream_t st,
+                       bool planar, bool fill) {
+  if (planar) return fill ? launch_qv<TIn, TOut, true, true>(src, out, a, n, st)
+                          : launch_qv<TIn, TOut, true, false>(src, out, a, n, st);
+  return fill ? launch_qv<TIn, TOut, false, true>(src, out, a, n, st)
+              : launch_qv<TIn, TOut, false, false>(src, out, a, n, st);
 }
 
 // dequantize: channel-last or planar integer frames -> channel-last values.
@@ -303,7 +483,7 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int6
                 const double *mins, const double *maxs, int32_t bit_depth, int32_t clamp,
                 int32_t fill_mode, float fill_value, int32_t seg_len, const float *seg_last,
                 const double *pca_mean, const double *pca_comps, int32_t n_pcs, int32_t out_layout,
-                int32_t pad_mode, void *out, uint32_t *err_word, void *stream) {
+                int32_t pad_mode, void *out, float *filled_out, uint32_t *err_word, void *stream) {
   if (!src || !out || !mins || !maxs) return fail(CV_ERR_ARG, "cv_quantize: null pointer");
   if (!valid_depth(bit_depth)) return fail(CV_ERR_ARG, "bit depth %d not in (8, 10, 12, 16)", bit_depth);
   if (C <= 0 || C > kMaxC) return fail(CV_ERR_UNSUPPORTED, "cv_quantize: %d channels (supported 1..%d)", C, kMaxC);
@@ -340,9 +520,23 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int6
   a.mins = mins;
   a.maxs = maxs;
   a.seg_last = seg_last;
+  a.filled_out = fill ? filled_out : nullptr;
   a.err = err_word;
   cudaStream_t st = (cudaStream_t)stream;
   const bool planar = out_layout == CV_LAYOUT_PLANAR;
+  const bool aligned = (((uintptr_t)src | (uintptr_t)out | (uintptr_t)filled_out) & 15) == 0;
+  if (!pca && aligned && ((HW * C) % 4 == 0)) {
+    const bool u8 = bit_depth == 8;
+    switch (dtype) {
+      case CV_F32: return u8 ? dispatch_qv<float, uint8_t>(src, out, a, n_cubes, st, planar, fill)
+                             : dispatch_qv<float, uint16_t>(src, out, a, n_cubes, st, planar, fill);
+      case CV_U16: return u8 ? dispatch_qv<uint16_t, uint8_t>(src, out, a, n_cubes, st, planar, false)
+                             : dispatch_qv<uint16_t, uint16_t>(src, out, a, n_cubes, st, planar, false);
+      case CV_U8: return u8 ? dispatch_qv<uint8_t, uint8_t>(src, out, a, n_cubes, st, planar, false)
+                            : dispatch_qv<uint8_t, uint16_t>(src, out, a, n_cubes, st, planar, false);
+      default: break;
+    }
+  }
   switch (dtype) {
     case CV_F32: return dispatch_q1<float>(src, out, a, p, n_cubes, st, pca, planar, fill);
     case CV_F64: return dispatch_q1<double>(src, out, a, p, n_cubes, st, pca, planar, false);

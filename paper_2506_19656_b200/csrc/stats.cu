@@ -10,6 +10,7 @@
 // segment, so each time step is one fully coalesced sweep of the chunk and the
 // per-element forward-fill carry lives in registers. NT is a multiple of C, so
 // a thread's band is tid % C for all its elements.
+#include <type_traits>
 #include "common.cuh"
 
 namespace cvb {
@@ -97,6 +98,122 @@ k_stats(const TIn *__restrict__ src, int64_t T, int64_t inner, int C, int fill_m
   commit_band_stats<Acc>(mn, mx, nanc, lead, C, ws + a * C, smem);
 }
 
+// Vectorised K1 for rows whose length is a multiple of 4 (16 B loads of f32,
+// 8 B of u16): thread lane j of a vector always sees band (4*tid + j) % C;
+// the next time step's vectors are in flight while the current one is reduced.
+template <typename TIn> struct SVec4T;
+template <> struct SVec4T<float> { using type = float4; };
+template <> struct SVec4T<uint16_t> { using type = ushort4; };
+
+template <typename TIn, int KV>
+__global__ void __launch_bounds__(1024)
+k_stats_vec(const TIn *__restrict__ src, int64_t T, int64_t inner, int C, int fill_mode,
+            int seg_len, StatsEntry *__restrict__ ws, float *__restrict__ seg_last, uint32_t *err) {
+  using V = typename SVec4T<TIn>::type;
+  constexpr int VEC = 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int64_t a = blockIdx.z, seg = blockIdx.y, nseg = gridDim.y;
+  const int64_t e0 = (int64_t)blockIdx.x * NT * VEC * KV;
+  const int64_t t0 = seg * seg_len;
+  const int64_t t1 = min(T, t0 + (int64_t)seg_len);
+  const TIn *cube = src + a * T * inner;
+  int64_t voff[KV];
+  bool vok[KV];
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    voff[k] = e0 + (int64_t)VEC * (tid + k * NT);
+    vok[k] = voff[k] < inner;
+  }
+  float mn[VEC], mx[VEC];
+  unsigned nanc[VEC];
+  bool lead[VEC];
+  float last[KV][VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    mn[j] = INFINITY;
+    mx[j] = -INFINITY;
+    nanc[j] = 0;
+    lead[j] = false;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) last[k][j] = __int_as_float(0x7fc00000);
+  }
+  bool inf_seen = false;
+  V cur[KV], nxt[KV];
+#pragma unroll
+  for (int k = 0; k < KV; ++k)
+    if (vok[k] && t0 < t1) cur[k] = __ldg(reinterpret_cast<const V *>(cube + t0 * inner + voff[k]));
+  for (int64_t t = t0; t < t1; ++t) {
+    if (t + 1 < t1) {
+#pragma unroll
+      for (int k = 0; k < KV; ++k)
+        if (vok[k]) nxt[k] = __ldg(reinterpret_cast<const V *>(cube + (t + 1) * inner + voff[k]));
+    }
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      if (!vok[k]) continue;
+      const float x[VEC] = {(float)cur[k].x, (float)cur[k].y, (float)cur[k].z, (float)cur[k].w};
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        // fminf/fmaxf skip NaN; infinities are flagged and kept out of the range
+        const bool nan = isnan(x[j]);
+        const bool inf = isinf(x[j]);
+        inf_seen |= inf;
+        const float v = inf ? mn[j] : x[j];
+        mn[j] = fminf(mn[j], v);
+        mx[j] = fmaxf(mx[j], inf ? mx[j] : x[j]);
+        nanc[j] += nan ? 1u : 0u;
+        lead[j] |= nan && (t == 0);
+        if (!nan && !inf) last[k][j] = x[j];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KV; ++k) cur[k] = nxt[k];
+  }
+  if (seg_last && t0 < t1) {
+    float *sl = seg_last + (a * nseg + seg) * inner;
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+      if (vok[k])
+        *reinterpret_cast<float4 *>(sl + voff[k]) = make_float4(last[k][0], last[k][1], last[k][2], last[k][3]);
+  }
+  flag_warp(err, inf_seen, CV_FLAG_NONFINITE);
+  unsigned tn = nanc[0] + nanc[1] + nanc[2] + nanc[3];
+  flag_warp(err, fill_mode == 0 && tn > 0, CV_FLAG_NAN);
+
+  // per-band reduction over the 4*NT (thread, lane) entries; entry i has band i % C
+  float *smn = reinterpret_cast<float *>(smem);
+  float *smx = smn + VEC * NT;
+  unsigned *snan = reinterpret_cast<unsigned *>(smx + VEC * NT);
+  unsigned *slead = snan + VEC * NT;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    smn[VEC * tid + j] = mn[j];
+    smx[VEC * tid + j] = mx[j];
+    snan[VEC * tid + j] = nanc[j];
+    slead[VEC * tid + j] = lead[j] ? 1u : 0u;
+  }
+  __syncthreads();
+  if (tid < C) {
+    float bmn = INFINITY, bmx = -INFINITY;
+    unsigned long long bn = 0;
+    unsigned bl = 0;
+    for (int i = tid; i < VEC * NT; i += C) {
+      bmn = fminf(bmn, smn[i]);
+      bmx = fmaxf(bmx, smx[i]);
+      bn += snan[i];
+      bl |= slead[i];
+    }
+    StatsEntry *en = ws + a * C + tid;
+    if (bmn <= bmx) {
+      atomicMin(&en->min_key, dkey((double)bmn));
+      atomicMax(&en->max_key, dkey((double)bmx));
+    }
+    if (bn) atomicAdd(&en->nan_count, bn);
+    if (bl) atomicOr(&en->lead, 1u);
+  }
+}
+
 __global__ void k_stats_finalize(const StatsEntry *__restrict__ ws, int64_t n, int fill_mode,
                                  float fill, double *mins, double *maxs, int64_t *nan_counts) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -172,8 +289,21 @@ static void launch_stats(const void *src, int64_t n, int64_t T, int64_t inner, i
                          cudaStream_t st) {
   using Acc = typename AccT<TIn>::type;
   const int NT = threads_for_channels(C);
-  const int64_t nchunk = (inner + (int64_t)NT * kStatsK - 1) / ((int64_t)NT * kStatsK);
   const int64_t nseg = (T + seg_len - 1) / seg_len;
+  if constexpr (std::is_same<TIn, float>::value || std::is_same<TIn, uint16_t>::value) {
+    constexpr int KV = 2;
+    if (inner % 4 == 0 && (((uintptr_t)src | (uintptr_t)seg_last) & 15) == 0) {
+      const int64_t nchunk = (inner + (int64_t)NT * 4 * KV - 1) / ((int64_t)NT * 4 * KV);
+      dim3 grid((unsigned)nchunk, (unsigned)nseg, (unsigned)n);
+      const size_t sm = (size_t)NT * 4 * 16;
+      if (sm > 48 * 1024)
+        cudaFuncSetAttribute(k_stats_vec<TIn, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_stats_vec<TIn, KV><<<grid, NT, sm, st>>>((const TIn *)src, T, inner, C, fill_mode, seg_len,
+                                                   (StatsEntry *)ws, seg_last, err);
+      return;
+    }
+  }
+  const int64_t nchunk = (inner + (int64_t)NT * kStatsK - 1) / ((int64_t)NT * kStatsK);
   dim3 grid((unsigned)nchunk, (unsigned)nseg, (unsigned)n);
   size_t sm = (size_t)NT * (2 * sizeof(Acc) + 2 * sizeof(unsigned));
   k_stats<TIn, kStatsK><<<grid, NT, sm, st>>>((const TIn *)src, T, inner, C, fill_mode, seg_len,

@@ -95,8 +95,8 @@ def score(orig, recon, want_ssim: bool = True):
     ssum = torch.zeros(C, dtype=torch.float64, device=d)
     lib = _lib.load()
     ws = dev.workspace(lib.cv_eval_ws_bytes(1, T, H, W, C, int(want_ssim)), d)
-    _lib.call("cv_eval", None, 0, C, None, None, 8, None, None, r.ptr, r.code, o.ptr, o.code, 0, 0.0,
-              1, None, 1, T, H, W, C, maxs.data_ptr(), int(want_ssim), None, ws.data_ptr(),
+    _lib.call("cv_eval", None, 0, C, None, None, 8, None, None, r.ptr, r.code, o.ptr, o.code,
+              1, T, H, W, C, maxs.data_ptr(), int(want_ssim), None, ws.data_ptr(),
               sse.data_ptr(), ssum.data_ptr(), err.ptr, dev.stream_ptr(d))
     if err.flags() & (_lib.CV_FLAG_NAN | _lib.CV_FLAG_NONFINITE):
         raise ConfigurationError("metrics need finite originals")

@@ -82,6 +82,7 @@ class Encoded:
     seg_last: torch.Tensor | None        # forward-fill carry map (scoring the filled cube)
     pca: list = field(default_factory=list)   # one PcaFold per cube
     err: dev.ErrWord | None = None
+    filled: torch.Tensor | None = None   # forward-filled cube (float32 sources)
 
     @property
     def n_encoded(self) -> int:
@@ -158,11 +159,13 @@ def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normaliz
     return _fold(eig_model(mean, cov, n_pcs, C)), g["mins"], g["maxs"]
 
 
-def encode_prep(cube, spec: StreamSpec, marks=None) -> Encoded:
+def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | None = None) -> Encoded:
     """Cube(s) -> planar integer frames + QuantParams (+ PCA models).
 
-    ``marks`` (optional callable) is invoked with a phase label after the
-    statistics phase; the benchmark uses it to record CUDA events.
+    Float32 cubes are forward-filled on the fly; the quantiser also writes the
+    filled cube (``Encoded.filled``, forward_fill_time's output) so decode can
+    score against what the codec saw. ``marks`` (optional callable) is invoked
+    with a phase label after the statistics phase (benchmark CUDA events).
     """
     x, (B, T, H, W, C) = _as_batch(cube)
     d = x.device
@@ -211,21 +214,26 @@ def encode_prep(cube, spec: StreamSpec, marks=None) -> Encoded:
     G = len(groups)
     tdt, _ = dev.out_dtype_for_depth(spec.bit_depth)
     frames = torch.empty((B, G, T, 3, HW), dtype=tdt, device=d)
+    filled = None
+    if spec.n_pcs == 0 and fill:
+        filled = filled_out if filled_out is not None else torch.empty_like(x.t)
     for b in range(B) if spec.n_pcs else [None]:
         if b is None:
             _lib.call("cv_quantize", x.ptr, x.code, B, T, HW, C, qmins.data_ptr(), qmaxs.data_ptr(),
                       spec.bit_depth, int(spec.clamp), int(fill), float(spec.fill_value), seg,
                       seg_last.data_ptr() if seg_last is not None else None, None, None, 0,
-                      _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames.data_ptr(), err.ptr, s)
+                      _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames.data_ptr(),
+                      filled.data_ptr() if filled is not None else None, err.ptr, s)
         else:
             fold = folds[b]
             src_b = x.t[b] if x.t.dim() == 5 else x.t
             _lib.call("cv_quantize", src_b.data_ptr(), x.code, 1, T, HW, C, qmins[b:].data_ptr(),
                       qmaxs[b:].data_ptr(), spec.bit_depth, int(spec.clamp), 0, 0.0, seg, None,
                       fold.fwd_mean.ctypes.data, fold.fwd_comps.ctypes.data, E,
-                      _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames[b].data_ptr(), err.ptr, s)
+                      _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames[b].data_ptr(), None,
+                      err.ptr, s)
     return Encoded(frames, qmins, qmaxs, spec, (B, T, H, W, C), groups, peaks, nans, seg_last,
-                   folds, err)
+                   folds, err, filled)
 
 
 @dataclass
@@ -259,11 +267,18 @@ class Scores:
         return out
 
 
-def decode_eval(enc: Encoded, orig, frames: torch.Tensor | None = None, want_ssim: bool = True,
-                want_recon: bool = True, recon_out: torch.Tensor | None = None, orig_arr=None):
-    """Frames (the codec's decoded output; default: ``enc.frames``) -> recon + scores."""
+def decode_eval(enc: Encoded, orig=None, frames: torch.Tensor | None = None, want_ssim: bool = True,
+                want_recon: bool = True, recon_out: torch.Tensor | None = None):
+    """Frames (the codec's decoded output; default: ``enc.frames``) -> recon + scores.
+
+    Scores are taken against the forward-filled original:
+    ``enc.filled`` when the encoder produced it, else ``orig``.
+    """
     B, T, H, W, C = enc.shape
-    o, shp = orig_arr if orig_arr is not None else _as_batch(orig)
+    ref = enc.filled if enc.filled is not None else orig
+    if ref is None:
+        raise ConfigurationError("decode_eval needs the original cube to score against")
+    o, shp = _as_batch(ref)
     if shp != enc.shape:
         raise ConfigurationError(f"original {shp} does not match the encoded stream {enc.shape}")
     if want_ssim and (H < SSIM_WINDOW or W < SSIM_WINDOW):
@@ -284,16 +299,12 @@ def decode_eval(enc: Encoded, orig, frames: torch.Tensor | None = None, want_ssi
     ws = dev.workspace(lib.cv_eval_ws_bytes(B, T, H, W, C, int(want_ssim)), d)
     err = enc.err if enc.err is not None else dev.ErrWord(d)
     fdt = _lib.CV_U8 if fr.dtype == torch.uint8 else _lib.CV_U16
-    fill = enc.seg_last is not None
     if not enc.pca:
         _lib.call("cv_eval", fr.data_ptr(), fdt, E, enc.qmins.data_ptr(), enc.qmaxs.data_ptr(),
-                  enc.spec.bit_depth, None, None, None, 0, o.ptr, o.code, int(fill),
-                  float(enc.spec.fill_value), enc.spec.seg_len,
-                  enc.seg_last.data_ptr() if fill else None, B, T, H, W, C, enc.peaks.data_ptr(),
-                  int(want_ssim), recon.data_ptr() if recon is not None else None, ws.data_ptr(),
-                  sse.data_ptr(), ssum.data_ptr(), err.ptr, s)
+                  enc.spec.bit_depth, None, None, None, 0, o.ptr, o.code, B, T, H, W, C,
+                  enc.peaks.data_ptr(), int(want_ssim), recon.data_ptr() if recon is not None else None,
+                  ws.data_ptr(), sse.data_ptr(), ssum.data_ptr(), err.ptr, s)
     else:
-        per_cube = T * H * W * C
         for b in range(B):
             fold = enc.pca[b]
             o_b = o.t[b] if o.t.dim() == 5 else o.t
@@ -302,10 +313,9 @@ def decode_eval(enc: Encoded, orig, frames: torch.Tensor | None = None, want_ssi
                 r_b = (recon[b] if recon.dim() == 5 else recon).data_ptr()
             _lib.call("cv_eval", fr[b].data_ptr(), fdt, E, enc.qmins[b:].data_ptr(),
                       enc.qmaxs[b:].data_ptr(), enc.spec.bit_depth, fold.inv_mean.ctypes.data,
-                      fold.inv_comps.ctypes.data, None, 0, o_b.data_ptr(), o.code, 0, 0.0, 1, None,
-                      1, T, H, W, C, enc.peaks[b:].data_ptr(), int(want_ssim), r_b, ws.data_ptr(),
+                      fold.inv_comps.ctypes.data, None, 0, o_b.data_ptr(), o.code, 1, T, H, W, C,
+                      enc.peaks[b:].data_ptr(), int(want_ssim), r_b, ws.data_ptr(),
                       sse[b:].data_ptr(), ssum[b:].data_ptr(), err.ptr, s)
-        del per_cube
     scores = Scores(sse, ssum, enc.peaks, T * H * W,
                     T * (H - SSIM_WINDOW + 1) * (W - SSIM_WINDOW + 1) if want_ssim else 0,
                     want_ssim, enc.frame_bytes // B, enc.shape)

@@ -151,7 +151,7 @@ def quantize(arr, params: QuantParams, clamp: bool = False):
         err = dev.ErrWord(x.device)
         _lib.call("cv_quantize", x.ptr, x.code, 1, T, H * W, C, mins.data_ptr(), maxs.data_ptr(),
                   params.bit_depth, int(bool(clamp)), 0, 0.0, _STATS_SEG, None, None, None, 0,
-                  _lib.CV_LAYOUT_CHANNEL_LAST, _lib.CV_PAD_REPEAT, out.data_ptr(), err.ptr,
+                  _lib.CV_LAYOUT_CHANNEL_LAST, _lib.CV_PAD_REPEAT, out.data_ptr(), None, err.ptr,
                   dev.stream_ptr(x.device))
         flags = err.flags()
         if flags & _lib.CV_FLAG_NAN:

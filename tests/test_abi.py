@@ -43,18 +43,18 @@ def test_validation_without_launch():
     lib = _lib.load()
     # bad bit depth: rejected before any CUDA call
     st = lib.cv_quantize(1, _lib.CV_F32, 1, 1, 1, 1, 1, 1, 9, 0, 0, 0.0, 16, None, None, None, 0,
-                         0, 0, 1, None, None)
+                         0, 0, 1, None, None, None)
     assert st == _lib.CV_ERR_ARG
     assert b"bit depth 9" in lib.cv_last_error()
     st = lib.cv_stats(1, _lib.CV_F32, 1, 4, 10, 3, 0, 16, 1, None, None, None)
     assert st == _lib.CV_ERR_SHAPE
     st = lib.cv_stats(1, _lib.CV_F32, 1, 4, 66, 33, 0, 16, 1, None, None, None)
     assert st == _lib.CV_ERR_UNSUPPORTED
-    st = lib.cv_eval(1, _lib.CV_U16, 3, 1, 1, 10, None, None, 1, _lib.CV_F32, 1, _lib.CV_F32, 0, 0.0,
-                     1, None, 1, 1, 8, 8, 3, 1, 1, None, 1, 1, 1, None, None)
+    st = lib.cv_eval(1, _lib.CV_U16, 3, 1, 1, 10, None, None, 1, _lib.CV_F32, 1, _lib.CV_F32,
+                     1, 1, 8, 8, 3, 1, 1, None, 1, 1, 1, None, None)
     assert st == _lib.CV_ERR_ARG  # both frames and recon_in
-    st = lib.cv_eval(None, 0, 3, None, None, 8, None, None, 1, _lib.CV_F32, 1, _lib.CV_F32, 0, 0.0,
-                     1, None, 1, 1, 8, 8, 3, 1, 1, None, 1, 1, 1, None, None)
+    st = lib.cv_eval(None, 0, 3, None, None, 8, None, None, 1, _lib.CV_F32, 1, _lib.CV_F32,
+                     1, 1, 8, 8, 3, 1, 1, None, 1, 1, 1, None, None)
     assert st == _lib.CV_ERR_SHAPE  # 8x8 frames < 11-px window
     # zero-size work is a no-op success without touching the device
     assert lib.cv_stats_finalize(1, 0, 3, 0, 0.0, None, None, None, None) == _lib.CV_OK

@@ -125,7 +125,9 @@ def test_quantize_random_vs_oracle(cuda, B):
     dq = G.dequantize(q, G.QuantParams(B, tuple(lo), tuple(hi)))
     np.testing.assert_array_equal(dq, O.dequantize(q, lo, hi, B))
     step = (hi - lo) / O.LEVELS[B]
-    assert (np.abs(dq - x) <= step / 2 * (1 + 1e-12) + 1e-300).all()
+    # exact-math bound step/2 plus the float64 rounding of the operands
+    slack = 8 * np.spacing(np.maximum(np.abs(x), np.maximum(np.abs(lo), np.abs(hi))).astype(np.float64))
+    assert (np.abs(dq - x) <= step / 2 + slack).all()
 
 
 def test_quantize_exhaustive_8bit(cuda):
