@@ -56,8 +56,8 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _deps())
 
 
-def _compile(nvcc: str, src: Path, extra: list[str]) -> Path:
-    obj = BUILD / (src.stem + ".o")
+def _compile(nvcc: str, src: Path, extra: list[str], build_dir: Path = BUILD) -> Path:
+    obj = build_dir / (src.stem + ".o")
     cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -65,30 +65,45 @@ def _compile(nvcc: str, src: Path, extra: list[str]) -> Path:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | None = None) -> Path:
-    """Compile the library if any source is newer than it; return its path."""
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, extra_flags: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Compile the library if any source is newer than it; return its path.
+
+    ``extra_flags`` / ``out`` build an experimental variant next to the
+    default library (e.g. a different launch-bounds setting for A/B runs).
+    """
+    lib = Path(out) if out else LIB
+    if not force and out is None and up_to_date():
         return LIB
     nvcc = _nvcc()
-    BUILD.mkdir(parents=True, exist_ok=True)
-    LIB.parent.mkdir(parents=True, exist_ok=True)
+    build_dir = BUILD if out is None else BUILD.parent / ("cvb200_" + lib.stem)
+    build_dir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     extra = list(extra_flags or [])
     srcs = sources()
     # compile the heaviest translation units first
     srcs.sort(key=lambda p: -p.stat().st_size)
     workers = max(1, min(len(srcs), os.cpu_count() or 4))
     with cf.ThreadPoolExecutor(workers) as ex:
-        objs = list(ex.map(lambda s: _compile(nvcc, s, extra), srcs))
-    tmp = LIB.with_suffix(".so.tmp")
+        objs = list(ex.map(lambda s: _compile(nvcc, s, extra, build_dir), srcs))
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    out = None
+    flags = []
+    for a in args:
+        if a.startswith("--out="):
+            out = Path(a.split("=", 1)[1])
+        elif a.startswith("-D"):
+            flags.append(a)
+    build(force="--force" in args or out is not None, verbose=True, extra_flags=flags, out=out)

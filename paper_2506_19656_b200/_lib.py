@@ -8,12 +8,13 @@ current torch CUDA stream handle.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from .errors import ConfigurationError
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libcvb200.so"
+LIB_PATH = Path(os.environ.get("CVB200_LIB", Path(__file__).resolve().parent / "lib" / "libcvb200.so"))
 
 # dtype / layout / status codes (mirror include/cvb200.h)
 CV_U8, CV_U16, CV_F32, CV_F64 = 0, 1, 2, 3

@@ -178,6 +178,43 @@ __device__ __forceinline__ uint32_t quantize_value(double v, const QBand &b) {
   return (uint32_t)q;
 }
 
+// Float32 fast path of the quantiser for float32 / integer sources.
+// x32 = RN32(fma(v, RN32(K), RN32(-m K))), K = L/span, satisfies
+//   |x32 + 0.5 - (x_ref + 0.5)| <= eps = 2^-24 (2L + 1 + 2 K A) + 2^-40 L,
+// A = max(|min|, |max|), for every in-range v (x_ref: the reference's float64
+// value). When frac(x32 + 0.5) is more than eps away from an integer the
+// floor is the reference's; otherwise the element takes the exact float64
+// path. Bands with eps > 2^-9 (huge offsets, 16-bit) always use float64.
+// Range checks use the float neighbours of min/max, exact for float v.
+struct QBand32 {
+  float k, b, eps, lo, hi;
+  bool use32;
+};
+
+__device__ __forceinline__ QBand32 make_qband32(const QBand &q, int clamp) {
+  QBand32 r;
+  const double K = q.L / q.s;
+  const double A = fmax(fabs(q.m), fabs(q.M));
+  const double eps = 5.9604644775390625e-08 * (2.0 * q.L + 1.0 + 2.0 * K * A) + 1e-12 * q.L;
+  r.k = (float)K;
+  r.b = (float)(-q.m * K);
+  r.eps = (float)eps;
+  r.lo = __double2float_ru(q.m);
+  r.hi = __double2float_rd(q.M);
+  r.use32 = !clamp && !q.constant && eps < 0.001953125;
+  return r;
+}
+
+// Returns true and the code in q when the float32 path decides the element.
+__device__ __forceinline__ bool quantize_fast32(float v, const QBand32 &b, uint32_t &q, bool &bad) {
+  const float t = fmaf(v, b.k, b.b) + 0.5f;
+  const float fl = floorf(t);
+  const float fr = t - fl;
+  bad |= (v < b.lo) || (v > b.hi);
+  q = (uint32_t)fminf(fmaxf(fl, 0.f), 65535.f);
+  return fr > b.eps && fr < 1.f - b.eps;
+}
+
 // RN(q / L) without a division: q0 = RN(q*rL), e = fma(-q0, L, q) (exact),
 // RN(q0 + e*rL). Equal to the IEEE quotient for every q in [0, L] at all four
 // bit depths (exhaustive proof: tests/test_exactness.py).

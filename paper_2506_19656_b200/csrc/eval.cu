@@ -23,6 +23,7 @@
 #include "pca_params.cuh"
 
 #include "eval_kernel.cuh"
+#include "ssim_kernel.cuh"
 
 namespace cvb {
 
@@ -61,6 +62,20 @@ static size_t eval_smem(int C, int E, int TX, bool ssim, bool pca) {
 template <typename TO, int RS>
 static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool ssim, int64_t n,
                         cudaStream_t st) {
+  if (ssim) {
+    const int ncg = (a.C + kSsimWarpsPerCta - 1) / kSsimWarpsPerCta;
+    const int wpc = a.C < kSsimWarpsPerCta ? a.C : kSsimWarpsPerCta;
+    dim3 grid((unsigned)(a.nstrips * ncg), (unsigned)a.T, (unsigned)n);
+    if constexpr (RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) {
+      if (pca) k_eval_ssim<TO, RS, true, false><<<grid, 32 * wpc, 0, st>>>(a, inv);
+      else if (std::is_same<TO, float>::value && a.W % 4 == 0)
+        k_eval_ssim<TO, RS, false, std::is_same<TO, float>::value><<<grid, 32 * wpc, 0, st>>>(a, inv);
+      else k_eval_ssim<TO, RS, false, false><<<grid, 32 * wpc, 0, st>>>(a, inv);
+    } else {
+      k_eval_ssim<TO, RS, false, false><<<grid, 32 * wpc, 0, st>>>(a, inv);
+    }
+    return check_launch("cv_eval(ssim)");
+  }
   const int NT = a.TX * a.C;
   dim3 grid((unsigned)a.nstrips, (unsigned)a.T, (unsigned)n);
   const size_t sm = eval_smem(a.C, a.E, a.TX, ssim, pca);

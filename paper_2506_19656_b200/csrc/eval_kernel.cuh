@@ -41,9 +41,7 @@ enum { RS_FRAMES_U8 = 0, RS_FRAMES_U16 = 1, RS_RECON_F32 = 2, RS_RECON_F64 = 3 }
 
 __host__ __device__ inline int eval_tx(int C, bool ssim) {
   if (!ssim) return C <= 8 ? 64 : 32;
-  if (C <= 2) return 64;
-  if (C <= 16) return 32;
-  return 16;
+  return 32;  // k_eval_ssim: one lane per output column
 }
 
 // Gaussian taps g[|k|], k = -5..5, sigma = 1.5, normalised (float32 of the
@@ -121,8 +119,13 @@ template <> struct RawT<RS_FRAMES_U8> { using type = uint8_t; };
 template <> struct RawT<RS_FRAMES_U16> { using type = uint16_t; };
 template <> struct RawT<RS_RECON_F32> { using type = float; };
 
+#ifndef CVB_EVAL_MAXT
+#define CVB_EVAL_MAXT 512
+#define CVB_EVAL_MINB 1
+#endif
+
 template <typename TO, int RS, bool PCA, bool SSIM>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(CVB_EVAL_MAXT, CVB_EVAL_MINB)
 k_eval(const EvalArgs args, const PcaParams inv) {
   using R = typename RawT<RS>::type;
   constexpr bool FRAMES = (RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16);

@@ -251,15 +251,19 @@ k_quantize_vec(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantA
   const int64_t t1 = min(T, t0 + (int64_t)args.seg_len);
   const TIn *cube = src + a * T * inner;
   TOut *sq = reinterpret_cast<TOut *>(smem);  // [2][C][P]
+  QBand *qtab = reinterpret_cast<QBand *>(smem + ((PLANAR ? 2 * (size_t)C * P * sizeof(TOut) : 0) + 15) / 16 * 16);
+  for (int j = tid; j < C; j += NT)
+    qtab[j] = make_qband(args.mins[a * C + j], args.maxs[a * C + j], args.bit_depth);
+  __syncthreads();
 
-  QBand qb[VEC];
+  QBand32 qb[VEC];
   int cj[VEC], pj[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
     const int el = VEC * tid + j;
     cj[j] = el % C;
     pj[j] = el / C;
-    qb[j] = make_qband(args.mins[a * C + cj[j]], args.maxs[a * C + cj[j]], args.bit_depth);
+    qb[j] = make_qband32(qtab[cj[j]], args.clamp);
   }
   int64_t voff[KV];
   bool vok[KV];
@@ -319,8 +323,11 @@ k_quantize_vec(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantA
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
         if constexpr (!FILL) nanbad |= isnan(x[j]);
-        const double d = range_prep((double)x[j], qb[j], args.clamp, bad);
-        q[j] = quantize_value(d, qb[j]);
+        if (!(qb[j].use32 && quantize_fast32(x[j], qb[j], q[j], bad))) {
+          const QBand b = qtab[cj[j]];
+          const double d = range_prep((double)x[j], b, args.clamp, bad);
+          q[j] = quantize_value(d, b);
+        }
       }
       if constexpr (PLANAR) {
 #pragma unroll
@@ -378,7 +385,8 @@ static int launch_qv(const void *src, void *out, const QuantArgs &args, int64_t 
   constexpr int KV = 2;
   const int NT = threads_for_channels(args.C);
   const int P = NT * 4 * KV / args.C;
-  const size_t sm = PLANAR ? 2 * (size_t)args.C * P * sizeof(TOut) : 0;
+  const size_t sm = ((PLANAR ? 2 * (size_t)args.C * P * sizeof(TOut) : 0) + 15) / 16 * 16 +
+                    (size_t)args.C * sizeof(QBand);
   auto kern = k_quantize_vec<TIn, TOut, PLANAR, FILL, KV>;
   if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid((unsigned)((args.HW + P - 1) / P), (unsigned)cv_num_segments(args.T, args.seg_len),
