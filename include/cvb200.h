@@ -114,11 +114,14 @@ int cv_stats_finalize(const void *stats_ws, int64_t n_cubes, int32_t C,
  * src/out: [n_outer][T][inner] f32 (time axis moved to position 1 by the
  * caller's strides); mask: same shape, 1 = observed (ValidityMask).
  * seg_last: carry map produced by cv_stats(fill_mode=1, seg_len) over the
- * same geometry (C = 1 is fine). Leading gaps take (float)fill_value.
+ * same geometry (C = 1 is fine). carry_in (nullable, [n_outer][inner], NaN =
+ * none): values carried in from earlier time shards (multi-GPU T-sharding).
+ * Leading gaps take (float)fill_value.
  */
 int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner,
                     float fill_value, int32_t seg_len, const float *seg_last,
-                    float *out, uint8_t *mask, uint32_t *err_word, void *stream);
+                    const float *carry_in, float *out, uint8_t *mask,
+                    uint32_t *err_word, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* K4 — quantisation into integer frames                                   */
@@ -136,7 +139,8 @@ int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner,
  * pointers (the model comes from the host eigh); they are passed to the
  * kernel by value and shared by all n_cubes.
  * mins/maxs: [n_cubes][E] float64.
- * fill_mode 1 forward-fills NaN along T using seg_last (see cv_stats);
+ * fill_mode 1 forward-fills NaN along T using seg_last (see cv_stats) and
+ * carry_in (nullable [n_cubes][HW*C]: carries from earlier time shards);
  * filled_out (nullable, f32 input only) then receives the filled cube, i.e.
  * forward_fill_time's output (cube.py:244-246), in the same pass.
  * out_layout CHANNEL_LAST: out [n_cubes][T][HW][E] (what quantize returns).
@@ -148,7 +152,8 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T,
                 int64_t HW, int32_t C, const double *mins, const double *maxs,
                 int32_t bit_depth, int32_t clamp, int32_t fill_mode,
                 float fill_value, int32_t seg_len, const float *seg_last,
-                const double *pca_mean, const double *pca_comps, int32_t n_pcs,
+                const float *carry_in, const double *pca_mean,
+                const double *pca_comps, int32_t n_pcs,
                 int32_t out_layout, int32_t pad_mode, void *out,
                 float *filled_out, uint32_t *err_word, void *stream);
 

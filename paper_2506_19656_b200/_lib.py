@@ -41,9 +41,9 @@ SIGNATURES = {
     "cv_stats_reset": ([_P, _I64, _I32, _P], _INT),
     "cv_stats": ([_P, _I32, _I64, _I64, _I64, _I32, _I32, _I32, _P, _P, _P, _P], _INT),
     "cv_stats_finalize": ([_P, _I64, _I32, _I32, _F32, _P, _P, _P, _P], _INT),
-    "cv_forward_fill": ([_P, _I64, _I64, _I64, _F32, _I32, _P, _P, _P, _P, _P], _INT),
+    "cv_forward_fill": ([_P, _I64, _I64, _I64, _F32, _I32, _P, _P, _P, _P, _P, _P], _INT),
     "cv_quantize": ([_P, _I32, _I64, _I64, _I64, _I32, _P, _P, _I32, _I32, _I32, _F32, _I32, _P,
-                     _P, _P, _I32, _I32, _I32, _P, _P, _P, _P], _INT),
+                     _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P], _INT),
     "cv_dequantize": ([_P, _I32, _I64, _I64, _I64, _I32, _I32, _P, _P, _I32, _P, _I32, _P, _P], _INT),
     "cv_gram_ws_bytes": ([_I64, _I32], _SZ),
     "cv_pca_gram": ([_P, _I32, _I64, _I32, _P, _P, _P, _P, _P], _INT),

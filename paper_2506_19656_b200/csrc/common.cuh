@@ -114,6 +114,25 @@ __device__ __forceinline__ void flag_warp(uint32_t *err, bool cond, uint32_t f) 
   if (m && (threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) flag(err, f);
 }
 
+// --------------------------------------------------------------- fill carries
+// Forward-fill value entering time segment `seg` for element e: the last
+// observation of an earlier local segment, else the carry handed over by
+// earlier time shards (carry_in, NaN = none; multi-GPU T-sharding), else the
+// leading fill constant (cube.py:236-242 semantics).
+__device__ __forceinline__ float segment_carry(const float *__restrict__ sl_cube, int64_t seg,
+                                               int64_t inner, int64_t e,
+                                               const float *__restrict__ carry_in_cube, float fill) {
+  for (int64_t s = seg - 1; s >= 0; --s) {
+    const float v = sl_cube[s * inner + e];
+    if (!isnan(v)) return v;
+  }
+  if (carry_in_cube) {
+    const float v = carry_in_cube[e];
+    if (!isnan(v)) return v;
+  }
+  return fill;
+}
+
 // --------------------------------------------------------------- fill lookback
 // Forward-fill value of element `e` at time t of cube `a` when src[t][e] is
 // NaN: walk back inside the current segment, then over the per-segment

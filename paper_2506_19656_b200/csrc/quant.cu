@@ -45,6 +45,7 @@ struct QuantArgs {
   int seg_len;
   const double *mins, *maxs;
   const float *seg_last;
+  const float *carry_in;  // [n_cubes][inner] carries from earlier time shards (nullable)
   float *filled_out;
   uint32_t *err;
 };
@@ -105,16 +106,9 @@ k_quantize(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs 
 #pragma unroll
     for (int k = 0; k < kQK; ++k) {
       const int64_t e = e0 + (int64_t)k * NT;
-      carry[k] = args.fill;
-      if (e < inner) {
-        for (int64_t s = seg - 1; s >= 0; --s) {
-          float v = sl[s * inner + e];
-          if (!isnan(v)) {
-            carry[k] = v;
-            break;
-          }
-        }
-      }
+      carry[k] = e < inner ? segment_carry(sl, seg, inner, e, args.carry_in ? args.carry_in + a * inner : nullptr,
+                                           args.fill)
+                           : args.fill;
     }
   }
 
@@ -278,18 +272,10 @@ k_quantize_vec(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantA
 #pragma unroll
     for (int k = 0; k < KV; ++k)
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        carry[k][j] = args.fill;
-        if (vok[k]) {
-          for (int64_t s = seg - 1; s >= 0; --s) {
-            const float v = sl[s * inner + voff[k] + j];
-            if (!isnan(v)) {
-              carry[k][j] = v;
-              break;
-            }
-          }
-        }
-      }
+      for (int j = 0; j < VEC; ++j)
+        carry[k][j] = vok[k] ? segment_carry(sl, seg, inner, voff[k] + j,
+                                             args.carry_in ? args.carry_in + a * inner : nullptr, args.fill)
+                             : args.fill;
   }
 
   V cur[KV], nxt[KV];
@@ -490,6 +476,7 @@ extern "C" {
 int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int64_t HW, int32_t C,
                 const double *mins, const double *maxs, int32_t bit_depth, int32_t clamp,
                 int32_t fill_mode, float fill_value, int32_t seg_len, const float *seg_last,
+                const float *carry_in,
                 const double *pca_mean, const double *pca_comps, int32_t n_pcs, int32_t out_layout,
                 int32_t pad_mode, void *out, float *filled_out, uint32_t *err_word, void *stream) {
   if (!src || !out || !mins || !maxs) return fail(CV_ERR_ARG, "cv_quantize: null pointer");
@@ -528,6 +515,7 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int6
   a.mins = mins;
   a.maxs = maxs;
   a.seg_last = seg_last;
+  a.carry_in = fill ? carry_in : nullptr;
   a.filled_out = fill ? filled_out : nullptr;
   a.err = err_word;
   cudaStream_t st = (cudaStream_t)stream;

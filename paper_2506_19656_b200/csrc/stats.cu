@@ -237,8 +237,8 @@ __global__ void k_stats_finalize(const StatsEntry *__restrict__ ws, int64_t n, i
 template <int K>
 __global__ void __launch_bounds__(256)
 k_forward_fill(const float *__restrict__ src, int64_t T, int64_t inner, float fill, int seg_len,
-               const float *__restrict__ seg_last, float *__restrict__ out,
-               uint8_t *__restrict__ mask, uint32_t *err) {
+               const float *__restrict__ seg_last, const float *__restrict__ carry_in,
+               float *__restrict__ out, uint8_t *__restrict__ mask, uint32_t *err) {
   const int NT = blockDim.x;
   const int64_t a = blockIdx.z;
   const int64_t seg = blockIdx.y;
@@ -248,20 +248,12 @@ k_forward_fill(const float *__restrict__ src, int64_t T, int64_t inner, float fi
   const int64_t t1 = min(T, t0 + (int64_t)seg_len);
   const float *cube = src + a * T * inner;
   const float *sl = seg_last + a * nseg * inner;
+  const float *ci = carry_in ? carry_in + a * inner : nullptr;
   float carry[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int64_t e = e0 + (int64_t)k * NT;
-    carry[k] = fill;
-    if (e < inner) {
-      for (int64_t s = seg - 1; s >= 0; --s) {
-        float v = sl[s * inner + e];
-        if (!isnan(v)) {
-          carry[k] = v;
-          break;
-        }
-      }
-    }
+    carry[k] = e < inner ? segment_carry(sl, seg, inner, e, ci, fill) : fill;
   }
   bool inf_seen = false;
   for (int64_t t = t0; t < t1; ++t) {
@@ -369,8 +361,8 @@ int cv_stats_finalize(const void *stats_ws, int64_t n_cubes, int32_t C, int32_t 
 }
 
 int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner, float fill_value,
-                    int32_t seg_len, const float *seg_last, float *out, uint8_t *mask,
-                    uint32_t *err_word, void *stream) {
+                    int32_t seg_len, const float *seg_last, const float *carry_in, float *out,
+                    uint8_t *mask, uint32_t *err_word, void *stream) {
   if (!src || !out || !mask || !seg_last) return fail(CV_ERR_ARG, "cv_forward_fill: null pointer");
   if (n_outer < 0 || T < 0 || inner < 0 || seg_len <= 0) return fail(CV_ERR_SHAPE, "cv_forward_fill: bad sizes");
   if (n_outer > 65535 || cv_num_segments(T, seg_len) > 65535)
@@ -381,7 +373,7 @@ int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner,
   dim3 grid((unsigned)((inner + NT * K - 1) / (NT * K)), (unsigned)cv_num_segments(T, seg_len),
             (unsigned)n_outer);
   k_forward_fill<K><<<grid, NT, 0, (cudaStream_t)stream>>>(src, T, inner, fill_value, seg_len,
-                                                            seg_last, out, mask, err_word);
+                                                            seg_last, carry_in, out, mask, err_word);
   return check_launch("cv_forward_fill");
 }
 

@@ -83,7 +83,7 @@ def forward_fill_time(arr, time_axis: int, fill_value_for_leading=0.0):
         err = dev.ErrWord(t.device)
         seg_last, _ = segment_carries(x, outer, T, inner, FILL_SEGMENT, err)
         _lib.call("cv_forward_fill", x.ptr, outer, T, inner, float(fill_value_for_leading),
-                  FILL_SEGMENT, seg_last.data_ptr(), out.data_ptr(), mask.data_ptr(), err.ptr,
+                  FILL_SEGMENT, seg_last.data_ptr(), None, out.data_ptr(), mask.data_ptr(), err.ptr,
                   dev.stream_ptr(t.device))
         if err.flags() & _lib.CV_FLAG_NONFINITE:
             raise ConfigurationError("array contains +/-inf; only NaN marks missing data")

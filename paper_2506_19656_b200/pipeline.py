@@ -83,6 +83,8 @@ class Encoded:
     pca: list = field(default_factory=list)   # one PcaFold per cube
     err: dev.ErrWord | None = None
     filled: torch.Tensor | None = None   # forward-filled cube (float32 sources)
+    t_total: int | None = None           # frames over all time shards (multi-GPU)
+    shard: object | None = None          # dist.TimeShard of a time-sharded stream
 
     @property
     def n_encoded(self) -> int:
@@ -137,15 +139,25 @@ def _fold(model: PcaModel, offset=None, scale=None) -> PcaFold:
                    np.ascontiguousarray(fwd_mean), np.ascontiguousarray(inv), offset, scale)
 
 
-def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normalize: bool):
-    """K2 pass (Gram + band stats) -> host eigh -> folded model; returns (fold, mins, maxs)."""
+def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normalize: bool,
+            shard=None):
+    """K2 pass (Gram + band stats) -> host eigh -> folded model; returns (fold, mins, maxs).
+
+    With a multi-rank ``shard`` the Gram partials and band ranges of all time
+    shards are combined first, so every rank fits the same model.
+    """
     n = T * HW
     view = dev.Arr(x.t[cube] if x.t.dim() == 5 else x.t, x.code, x.host, x.np_dtype, (T, HW, C))
     g = gram(view, n, C, stats=True)
     if g["err"].flags() & (_lib.CV_FLAG_NAN | _lib.CV_FLAG_NONFINITE):
         raise ConfigurationError("cannot fit a PCA on non-finite values")
-    out = g["out"].cpu().numpy()
-    shift = g["shift"].double().cpu().numpy()
+    if shard is not None and shard.world > 1:
+        shift, out, n = shard.combine_gram(g["shift"], g["out"], n, C)
+        gmins, gmaxs = shard.combine_minmax(g["mins"], g["maxs"])
+        g["mins"], g["maxs"] = gmins, gmaxs
+    else:
+        out = g["out"].cpu().numpy()
+        shift = g["shift"].double().cpu().numpy()
     mins = g["mins"].cpu().numpy()
     maxs = g["maxs"].cpu().numpy()
     mean, cov = covariance_from_gram(shift, out, n, C)
@@ -159,7 +171,8 @@ def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normaliz
     return _fold(eig_model(mean, cov, n_pcs, C)), g["mins"], g["maxs"]
 
 
-def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | None = None) -> Encoded:
+def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | None = None,
+                shard=None) -> Encoded:
     """Cube(s) -> planar integer frames + QuantParams (+ PCA models).
 
     Float32 cubes are forward-filled on the fly; the quantiser also writes the
@@ -177,14 +190,24 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
     fill = x.code == _lib.CV_F32
     seg = spec.seg_len
     lib = _lib.load()
+    sharded = shard is not None and shard.world > 1
+    carry_in = None
     if spec.n_pcs == 0:
         E = C
         seg_last = None
         if fill:
             nseg = lib.cv_num_segments(T, seg)
             seg_last = torch.empty((B, nseg, HW * C), dtype=torch.float32, device=d)
-        qmins, qmaxs, nans = band_stats(x, B, T, HW * C, C, fill_mode=int(fill), seg_len=seg,
-                                        fill_value=spec.fill_value, err=err, seg_last=seg_last)
+        if not sharded:
+            qmins, qmaxs, nans = band_stats(x, B, T, HW * C, C, fill_mode=int(fill), seg_len=seg,
+                                            fill_value=spec.fill_value, err=err, seg_last=seg_last)
+        else:
+            from .dist import last_observed, raw_band_stats
+
+            mins, maxs, lead, nans = raw_band_stats(x, B, T, HW * C, C, int(fill), seg, err, seg_last)
+            qmins, qmaxs, nans = shard.combine_band_stats(mins, maxs, lead, nans, spec.fill_value)
+            if fill:
+                carry_in = shard.carry_in(last_observed(seg_last))
         peaks = qmaxs
         folds = []
     else:
@@ -197,7 +220,7 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
         qmaxs = torch.empty_like(qmins)
         peaks = torch.empty((B, C), dtype=torch.float64, device=d)
         for b in range(B):
-            fold, bmins, bmaxs = fit_pca(x, b, T, HW, C, E, spec.normalize)
+            fold, bmins, bmaxs = fit_pca(x, b, T, HW, C, E, spec.normalize, shard)
             folds.append(fold)
             peaks[b] = bmaxs
             sws = dev.workspace(lib.cv_stats_ws_bytes(1, E), d)
@@ -208,6 +231,8 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
                       sws.data_ptr(), err.ptr, s)
             _lib.call("cv_stats_finalize", sws.data_ptr(), 1, E, 0, 0.0, qmins[b:].data_ptr(),
                       qmaxs[b:].data_ptr(), None, s)
+            if sharded:
+                qmins[b], qmaxs[b] = shard.combine_minmax(qmins[b], qmaxs[b])
     if marks is not None:
         marks("stats")
     groups = pack_groups(E)
@@ -221,19 +246,26 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
         if b is None:
             _lib.call("cv_quantize", x.ptr, x.code, B, T, HW, C, qmins.data_ptr(), qmaxs.data_ptr(),
                       spec.bit_depth, int(spec.clamp), int(fill), float(spec.fill_value), seg,
-                      seg_last.data_ptr() if seg_last is not None else None, None, None, 0,
+                      seg_last.data_ptr() if seg_last is not None else None,
+                      carry_in.data_ptr() if carry_in is not None else None, None, None, 0,
                       _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames.data_ptr(),
                       filled.data_ptr() if filled is not None else None, err.ptr, s)
         else:
             fold = folds[b]
             src_b = x.t[b] if x.t.dim() == 5 else x.t
             _lib.call("cv_quantize", src_b.data_ptr(), x.code, 1, T, HW, C, qmins[b:].data_ptr(),
-                      qmaxs[b:].data_ptr(), spec.bit_depth, int(spec.clamp), 0, 0.0, seg, None,
+                      qmaxs[b:].data_ptr(), spec.bit_depth, int(spec.clamp), 0, 0.0, seg, None, None,
                       fold.fwd_mean.ctypes.data, fold.fwd_comps.ctypes.data, E,
                       _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames[b].data_ptr(), None,
                       err.ptr, s)
-    return Encoded(frames, qmins, qmaxs, spec, (B, T, H, W, C), groups, peaks, nans, seg_last,
-                   folds, err, filled)
+    enc = Encoded(frames, qmins, qmaxs, spec, (B, T, H, W, C), groups, peaks, nans, seg_last,
+                  folds, err, filled)
+    if sharded:
+        tt = torch.tensor([T], dtype=torch.int64, device=d)
+        shard.all_reduce(tt)
+        enc.t_total = int(tt.item())
+        enc.shard = shard
+    return enc
 
 
 @dataclass
@@ -316,9 +348,13 @@ def decode_eval(enc: Encoded, orig=None, frames: torch.Tensor | None = None, wan
                       fold.inv_comps.ctypes.data, None, 0, o_b.data_ptr(), o.code, 1, T, H, W, C,
                       enc.peaks[b:].data_ptr(), int(want_ssim), r_b, ws.data_ptr(),
                       sse[b:].data_ptr(), ssum[b:].data_ptr(), err.ptr, s)
-    scores = Scores(sse, ssum, enc.peaks, T * H * W,
-                    T * (H - SSIM_WINDOW + 1) * (W - SSIM_WINDOW + 1) if want_ssim else 0,
-                    want_ssim, enc.frame_bytes // B, enc.shape)
+    Tg = T
+    if enc.shard is not None and enc.t_total is not None:
+        sse, ssum = enc.shard.combine_scores(sse, ssum)  # per-band partial sums of all time shards
+        Tg = enc.t_total
+    scores = Scores(sse, ssum, enc.peaks, Tg * H * W,
+                    Tg * (H - SSIM_WINDOW + 1) * (W - SSIM_WINDOW + 1) if want_ssim else 0,
+                    want_ssim, enc.frame_bytes // B * Tg // T, (B, Tg, H, W, C))
     return recon, scores
 
 

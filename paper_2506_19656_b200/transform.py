@@ -150,7 +150,7 @@ def quantize(arr, params: QuantParams, clamp: bool = False):
         mins, maxs = _params_device(params, x.device)
         err = dev.ErrWord(x.device)
         _lib.call("cv_quantize", x.ptr, x.code, 1, T, H * W, C, mins.data_ptr(), maxs.data_ptr(),
-                  params.bit_depth, int(bool(clamp)), 0, 0.0, _STATS_SEG, None, None, None, 0,
+                  params.bit_depth, int(bool(clamp)), 0, 0.0, _STATS_SEG, None, None, None, None, 0,
                   _lib.CV_LAYOUT_CHANNEL_LAST, _lib.CV_PAD_REPEAT, out.data_ptr(), None, err.ptr,
                   dev.stream_ptr(x.device))
         flags = err.flags()

@@ -42,8 +42,8 @@ def test_version_and_strings():
 def test_validation_without_launch():
     lib = _lib.load()
     # bad bit depth: rejected before any CUDA call
-    st = lib.cv_quantize(1, _lib.CV_F32, 1, 1, 1, 1, 1, 1, 9, 0, 0, 0.0, 16, None, None, None, 0,
-                         0, 0, 1, None, None, None)
+    st = lib.cv_quantize(1, _lib.CV_F32, 1, 1, 1, 1, 1, 1, 9, 0, 0, 0.0, 16, None, None, None, None,
+                         0, 0, 0, 1, None, None, None)
     assert st == _lib.CV_ERR_ARG
     assert b"bit depth 9" in lib.cv_last_error()
     st = lib.cv_stats(1, _lib.CV_F32, 1, 4, 10, 3, 0, 16, 1, None, None, None)
