@@ -365,6 +365,45 @@ k_quantize_vec(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantA
   flag_warp(args.err, nanbad, CV_FLAG_NAN);
 }
 
+}  // namespace cvb
+
+#include "quant_planar.cuh"
+
+namespace cvb {
+
+template <typename TIn, typename TOut, bool FILL, bool PCA>
+static int launch_qp(const void *src, void *out, const QuantArgs &args, const PcaParams &pca,
+                     int64_t n_cubes, cudaStream_t st) {
+  constexpr int VE = 16 / sizeof(TIn);
+  const int NT = 256;
+  const int NE = NT * args.C;
+  const int SP = (NE + VE - 1) / VE * VE;
+  const size_t sm = (size_t)kQStages * SP * sizeof(TIn) + kMaxC * (sizeof(QBand) + sizeof(QBand32));
+  dim3 grid((unsigned)((args.HW + NT - 1) / NT), (unsigned)cv_num_segments(args.T, args.seg_len),
+            (unsigned)n_cubes);
+  const int mv = (args.C + VE - 1) / VE;  // vectors per thread per step
+#define CV_QP(MV)                                                                                     \
+  do {                                                                                                \
+    auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, MV>;                                          \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
+  } while (0)
+  if (mv <= 2) CV_QP(2);
+  else if (mv <= 4) CV_QP(4);
+  else CV_QP(8);
+#undef CV_QP
+  return check_launch("cv_quantize(planar)");
+}
+
+template <typename TIn, typename TOut>
+static int dispatch_qp(const void *src, void *out, const QuantArgs &a, const PcaParams &p, int64_t n,
+                       cudaStream_t st, bool pca, bool fill) {
+  if (pca) return fill ? launch_qp<TIn, TOut, true, true>(src, out, a, p, n, st)
+                       : launch_qp<TIn, TOut, false, true>(src, out, a, p, n, st);
+  return fill ? launch_qp<TIn, TOut, true, false>(src, out, a, p, n, st)
+              : launch_qp<TIn, TOut, false, false>(src, out, a, p, n, st);
+}
+
 template <typename TIn, typename TOut, bool PLANAR, bool FILL>
 static int launch_qv(const void *src, void *out, const QuantArgs &args, int64_t n_cubes,
                      cudaStream_t st) {
@@ -521,6 +560,18 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int6
   cudaStream_t st = (cudaStream_t)stream;
   const bool planar = out_layout == CV_LAYOUT_PLANAR;
   const bool aligned = (((uintptr_t)src | (uintptr_t)out | (uintptr_t)filled_out) & 15) == 0;
+  const int esz = dtype == CV_F32 ? 4 : dtype == CV_U16 ? 2 : dtype == CV_U8 ? 1 : 8;
+  if (planar && aligned && esz <= 4 && ((HW * C * esz) % 16 == 0) && C * 256 * esz <= 16384) {
+    const bool u8 = bit_depth == 8;
+    switch (dtype) {
+      case CV_F32: return u8 ? dispatch_qp<float, uint8_t>(src, out, a, p, n_cubes, st, pca, fill)
+                             : dispatch_qp<float, uint16_t>(src, out, a, p, n_cubes, st, pca, fill);
+      case CV_U16: return u8 ? dispatch_qp<uint16_t, uint8_t>(src, out, a, p, n_cubes, st, pca, false)
+                             : dispatch_qp<uint16_t, uint16_t>(src, out, a, p, n_cubes, st, pca, false);
+      default: return u8 ? dispatch_qp<uint8_t, uint8_t>(src, out, a, p, n_cubes, st, pca, false)
+                         : dispatch_qp<uint8_t, uint16_t>(src, out, a, p, n_cubes, st, pca, false);
+    }
+  }
   if (!pca && aligned && ((HW * C) % 4 == 0)) {
     const bool u8 = bit_depth == 8;
     switch (dtype) {

@@ -1,0 +1,187 @@
+// K4 planar quantiser (the encode-prep kernel of the benchmark).
+//
+// A CTA owns P = blockDim.x pixels of one cube for one time segment. Each time
+// step's source chunk (P*C contiguous elements) streams through a 4-stage
+// cp.async ring in shared memory (16-byte copies, 3 steps ahead). Per step:
+//   1. every thread forward-fills the vectors it copied (carries stay in
+//      registers: the thread <-> element ownership is fixed across steps),
+//      writes them back in place and to the filled cube (16-byte stores);
+//   2. barrier; thread p takes pixel p: reads its C values from shared memory,
+//      (projects them onto the PCA components), quantises each band with the
+//      float32 fast path / exact float64 fallback, and writes its sample of
+//      every plane of the planar frames (coalesced across the warp).
+#pragma once
+#include "common.cuh"
+#include "pca_params.cuh"
+
+namespace cvb {
+
+constexpr int kQStages = 4;
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_q() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_q() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV>
+__global__ void __launch_bounds__(256)
+k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs args,
+                  const PcaParams pca) {
+  constexpr int VE = 16 / sizeof(TIn);  // elements per 16-byte copy
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int C = args.C, E = args.E;
+  const int64_t T = args.T, HW = args.HW, inner = HW * C;
+  const int P = NT;
+  const int NE = P * C;                     // elements per full chunk
+  const int64_t a = blockIdx.z, seg = blockIdx.y, nseg = gridDim.y;
+  const int64_t pix0 = (int64_t)blockIdx.x * P;
+  const int64_t e0 = pix0 * C;
+  const int npix = (int)min((int64_t)P, HW - pix0);
+  const int ne = npix * C;
+  const int nvec = (ne + VE - 1) / VE;      // whole row end is vector aligned (host check)
+  const int64_t t0 = seg * args.seg_len;
+  const int64_t t1 = min(T, t0 + (int64_t)args.seg_len);
+  const TIn *cube = src + a * T * inner;
+  TIn *stage = reinterpret_cast<TIn *>(smem);  // [kQStages][NE + pad]
+  const int SP = (NE + VE - 1) / VE * VE;       // stage pitch (elements)
+  QBand *qtab = reinterpret_cast<QBand *>(smem + (size_t)kQStages * SP * sizeof(TIn));
+  QBand32 *qtab32 = reinterpret_cast<QBand32 *>(qtab + kMaxC);
+  for (int j = tid; j < E; j += NT) {
+    qtab[j] = make_qband(args.mins[a * E + j], args.maxs[a * E + j], args.bit_depth);
+    qtab32[j] = make_qband32(qtab[j], args.clamp);
+  }
+  __syncthreads();
+
+  // vectors owned by this thread: v = tid + i*NT (fixed across steps), at most
+  // MAXV = ceil(C / VE) (host-selected bound)
+  const int nv_mine = nvec > tid ? (nvec - tid + NT - 1) / NT : 0;
+
+  float carry[FILL ? MAXV * 4 : 1];
+  if constexpr (FILL) {
+    const float *sl = args.seg_last + a * nseg * inner;
+    const float *ci = args.carry_in ? args.carry_in + a * inner : nullptr;
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int el = (tid + i * NT) * 4 + j;
+        carry[i * 4 + j] = (i < nv_mine && el < ne) ? segment_carry(sl, seg, inner, e0 + el, ci, args.fill) : args.fill;
+      }
+  }
+
+  auto issue = [&](int64_t t) {
+    TIn *st = stage + (size_t)(t % kQStages) * SP;
+    const TIn *row = cube + t * inner + e0;
+    for (int i = 0; i < nv_mine; ++i) {
+      const int v = tid + i * NT;
+      cp_async16(st + v * VE, row + (int64_t)v * VE);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < kQStages - 1; ++s) {
+    if (t0 + s < t1) issue(t0 + s);
+    cp_async_commit_q();
+  }
+
+  // per-pixel constants
+  const int p = tid;
+  const bool pvalid = p < npix;
+  bool bad = false, nanbad = false;
+  TOut *obase = out + (a * args.G * T) * 3 * HW + pix0 + p;
+
+  for (int64_t t = t0; t < t1; ++t) {
+    cp_async_wait_q<kQStages - 2>();
+    TIn *st = stage + (size_t)(t % kQStages) * SP;
+    if constexpr (FILL) {
+      // forward fill of the owned vectors, in place, + the filled cube
+      float *fo = args.filled_out ? args.filled_out + (a * T + t) * inner + e0 : nullptr;
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        if (i < nv_mine) {
+          const int v = tid + i * NT;
+          float4 x = *reinterpret_cast<float4 *>(st + v * 4);
+          float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (isnan(xv[j])) xv[j] = carry[i * 4 + j];
+            else carry[i * 4 + j] = xv[j];
+          }
+          x = make_float4(xv[0], xv[1], xv[2], xv[3]);
+          *reinterpret_cast<float4 *>(st + v * 4) = x;
+          if (fo) *reinterpret_cast<float4 *>(fo + v * 4) = x;
+        }
+      }
+    }
+    __syncthreads();
+    // refill the stage consumed one step ago (every thread is past it now)
+    if (t + kQStages - 1 < t1) issue(t + kQStages - 1);
+    cp_async_commit_q();
+    if (pvalid) {
+      const TIn *px = st + p * C;
+      TOut *o = obase + t * 3 * HW;
+      if constexpr (!PCA) {
+        uint32_t last = 0;
+        const int64_t gstride = 3 * T * HW;  // next video (group of three planes)
+        for (int g = 0; g < args.G; ++g) {
+#pragma unroll
+          for (int jp = 0; jp < 3; ++jp) {
+            const int c = 3 * g + jp;
+            uint32_t q;
+            if (c < C) {
+              const float v = (float)px[c];
+              if constexpr (!FILL) nanbad |= (v != v);
+              const QBand32 b32 = qtab32[c];
+              if (!(b32.use32 && quantize_fast32(v, b32, q, bad))) {
+                const QBand b = qtab[c];
+                const double d = range_prep((double)v, b, args.clamp, bad);
+                q = quantize_value(d, b);
+              }
+              last = q;
+            } else {
+              q = args.pad_mode == CV_PAD_REPEAT ? last : 0u;
+            }
+            o[jp * HW] = (TOut)q;
+          }
+          o += gstride;
+        }
+      } else {
+        double d[kMaxC];
+#pragma unroll
+        for (int c = 0; c < kMaxC; ++c)
+          if (c < C) d[c] = __dsub_rn((double)px[c], pca.mean[c]);
+        uint32_t last = 0;
+        const int64_t gstride = 3 * T * HW;
+        for (int g = 0; g < args.G; ++g) {
+#pragma unroll
+          for (int jp = 0; jp < 3; ++jp) {
+            const int j = 3 * g + jp;
+            uint32_t q;
+            if (j < E) {
+              const double pc = project_one(d, pca, j);
+              const QBand b = qtab[j];
+              const double dv = range_prep(pc, b, args.clamp, bad);
+              q = quantize_value(dv, b);
+              last = q;
+            } else {
+              q = args.pad_mode == CV_PAD_REPEAT ? last : 0u;
+            }
+            o[jp * HW] = (TOut)q;
+          }
+          o += gstride;
+        }
+      }
+    }
+  }
+  cp_async_wait_q<0>();
+  flag_warp(args.err, bad, CV_FLAG_RANGE);
+  flag_warp(args.err, nanbad, CV_FLAG_NAN);
+}
+
+}  // namespace cvb
