@@ -328,6 +328,7 @@ def run_ours(a):
     shard = TimeShard() if wl.sharded else None
     recon = torch.empty(x.shape, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    wsp = pipeline.Workspace()
 
     phases = ("stats", "quantize", "eval")
     ev = []
@@ -345,7 +346,7 @@ def run_ours(a):
                 e.record(stream)
                 marks[label] = e
 
-        enc = pipeline.encode_prep(x, spec, marks=mark, shard=shard)
+        enc = pipeline.encode_prep(x, spec, marks=mark, shard=shard, workspace=wsp)
         mark("quantize")
         _, sc = pipeline.decode_eval(enc, x, recon_out=recon, want_ssim=wl.ssim)
         mark("eval")

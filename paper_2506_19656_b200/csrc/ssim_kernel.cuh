@@ -93,7 +93,6 @@ k_eval_ssim(const EvalArgs args, const PcaParams inv) {
     fbase = reinterpret_cast<const R *>(args.frames) + (((a * args.G + c / 3) * T + t) * 3 + c % 3) * HW;
   const R *pcbase = nullptr;
   if constexpr (PCA) pcbase = reinterpret_cast<const R *>(args.frames) + (a * args.G * T + t) * 3 * HW;
-  float *wp = (args.recon_out && mimg) ? args.recon_out + (a * T + t) * inner + xm * C + c : nullptr;
 
   // ---- raw input streams
   // ASYNC ring: raw_o[s][5+l] = original of main lane l, raw_o[s][pin_h] = halo;
@@ -104,16 +103,34 @@ k_eval_ssim(const EvalArgs args, const PcaParams inv) {
   const bool fcopy = lane < fwords;
   const int64_t fx = xf0 + (int64_t)lane * FPW;       // first pixel of this lane's word
   const bool fok = fcopy && fx >= 0 && fx + FPW <= W;
-  auto issue = [&](int64_t y) {
+  // running source pointers of the next row to copy (rows are issued in order)
+  const char *ip_m = reinterpret_cast<const char *>(obase + xmc * C);
+  const char *ip_h = reinterpret_cast<const char *>(obase + xhc * C);
+  const char *ip_f = fbase ? reinterpret_cast<const char *>(fbase + (fok ? fx : 0)) : nullptr;
+  const int64_t ostride = rowlen * (int64_t)sizeof(TO), fstride = W * (int64_t)sizeof(R);
+  // shared-memory byte addresses of this lane's slots in stage 0 (stage pitch below)
+  const uint32_t sa_m = smem_u32(&sh.raw_o[w][0][HALO + lane]);
+  const uint32_t sa_h = smem_u32(&sh.raw_o[w][0][pin_h]);
+  const uint32_t sa_f = smem_u32(&sh.raw_f[w][0][lane]);
+  constexpr uint32_t kPitchO = kRawO * sizeof(float), kPitchF = (kRawF / 2) * sizeof(uint32_t);
+  auto issue = [&](int y) {
     if constexpr (ASYNC) {
-      const int s = (int)(y & (kStages - 1));
-      if (mimg) cp_async4(&sh.raw_o[w][s][HALO + lane], obase + y * rowlen + xm * C);
-      if (himg) cp_async4(&sh.raw_o[w][s][pin_h], obase + y * rowlen + xh * C);
-      if (fok) cp_async4(&sh.raw_f[w][s][lane], fbase + y * W + fx);
+      const uint32_t s = (uint32_t)y & (kStages - 1);
+      if (mimg)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_m + s * kPitchO), "l"(ip_m) : "memory");
+      if (himg)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_h + s * kPitchO), "l"(ip_h) : "memory");
+      if (fok)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + s * kPitchF), "l"(ip_f) : "memory");
+      ip_m += ostride;
+      ip_h += ostride;
+      ip_f += fstride;
     }
   };
-  auto frame_at = [&](int s, int64_t x) -> uint32_t {
-    const int i = min(max((int)(x - xf0), 0), kRawF - 1);  // masked lanes read any valid slot
+  // frame sample of pixel x in stage s; masked lanes read any valid slot
+  const int fi_m = min(max((int)(xm - xf0), 0), kRawF - 1);
+  const int fi_h = min(max((int)(xh - xf0), 0), kRawF - 1);
+  auto frame_at = [&](int s, int i) -> uint32_t {
     const uint32_t word = sh.raw_f[w][s][i / FPW];
     if constexpr (FPW == 2) return (word >> (16 * (i & 1))) & 0xffffu;
     else return (word >> (8 * (i & 3))) & 0xffu;
@@ -177,7 +194,7 @@ k_eval_ssim(const EvalArgs args, const PcaParams inv) {
   if constexpr (ASYNC) {
 #pragma unroll
     for (int r = 0; r < kStages - 1; ++r) {
-      if (r < H) issue(r);
+      if (r < (int)H) issue(r);
       cp_async_commit();
     }
   } else {
@@ -188,25 +205,49 @@ k_eval_ssim(const EvalArgs args, const PcaParams inv) {
     r_h = r_hn;
   }
 
-  auto do_row = [&](int64_t y, auto ucst) {
+  const int H32 = (int)H;
+  const bool wr = args.recon_out != nullptr && mimg;
+  float *wq = (args.recon_out ? args.recon_out : reinterpret_cast<float *>(0)) + (a * T + t) * inner + xmc * C + c;
+
+  // horizontal 11-tap filter of a converted row + vertical ring step + SSIM of row y-5
+  auto filter_row = [&](int b, int y, auto ucst) {
     constexpr int U = decltype(ucst)::value;
-    constexpr int B = U & 1;  // row buffer (alternates; see the block note below)
+    float hs = 0.f, hd = 0.f, hss = 0.f, hdd = 0.f;
+#pragma unroll
+    for (int k = 0; k < kSsimTaps; ++k) {
+      const float4 v = srow[b][lane + k];
+      const float wt = gtap(k < kSsimRadius ? kSsimRadius - k : k - kSsimRadius);
+      hs = fmaf(wt, v.x, hs);
+      hd = fmaf(wt, v.y, hd);
+      hss = fmaf(wt, v.z, hss);
+      hdd = fmaf(wt, v.w, hdd);
+    }
+    float os, odv, oss, odd;
+    ring_step<U>(ring, hs, hd, hss, hdd, os, odv, oss, odd);
+    if (y >= 2 * kSsimRadius && col_valid) ssum += ssim_px(os, odv, oss, odd, c0, C1, C2);
+  };
+
+  auto do_row = [&](int y, auto ucst) {
+    constexpr int U = decltype(ucst)::value;
+    const int B = y & 1;  // row buffer: row y converts into B while row y-1 is filtered from B^1
     float om, oh = 0.f;
     double rm, rh = 0.0;
     if constexpr (ASYNC) {
-      if (y + kStages - 1 < H) issue(y + kStages - 1);
+      if (y + kStages - 1 < H32) issue(y + kStages - 1);
       cp_async_commit();
       cp_async_wait<kStages - 1>();
       __syncwarp();
-      const int s = (int)(y & (kStages - 1));
-      om = mimg ? sh.raw_o[w][s][HALO + lane] : 0.f;
-      rm = recon_raw(frame_at(s, xm), mimg);
+      const int s = y & (kStages - 1);
+      const float vm = sh.raw_o[w][s][HALO + lane];
+      om = mimg ? vm : 0.f;  // never-copied slots may hold NaN bits
+      rm = recon_raw(frame_at(s, fi_m), mimg);
       if (hact) {
-        oh = himg ? sh.raw_o[w][s][pin_h] : 0.f;
-        rh = recon_raw(frame_at(s, xh), himg);
+        const float vh = sh.raw_o[w][s][pin_h];
+        oh = himg ? vh : 0.f;
+        rh = recon_raw(frame_at(s, fi_h), himg);
       }
     } else {
-      if (y + 1 < H) load_next();
+      if (y + 1 < H32) load_next();
       om = (float)o_m;
       if constexpr (PCA) rm = recon_pca(y, xmc);
       else if constexpr (FRAMES) rm = recon_raw((uint32_t)r_m, true);
@@ -219,39 +260,28 @@ k_eval_ssim(const EvalArgs args, const PcaParams inv) {
       }
     }
     {
-      const double od = sizeof(TO) == 8 ? (double)o_m : (double)om;
-      const double diff = __dsub_rn(ASYNC ? (double)om : od, rm);
-      if (mimg) {
-        sse = __fma_rn(diff, diff, sse);
-        if (wp) {
-          *wp = (float)rm;
-          wp += rowlen;
-        }
-      }
-      const float d = (float)diff * mmask;
-      const float sv = fmaf(2.f, om - c0, -d) * mmask;
+      const double od = (sizeof(TO) == 8 && !ASYNC) ? (double)o_m : (double)om;
+      const double diff = __dsub_rn(od, rm);
+      if (mimg) sse = __fma_rn(diff, diff, sse);
+      if (wr) *wq = (float)rm;
+      wq += rowlen;
+      const float d = mimg ? (float)diff : 0.f;
+      const float sv = mimg ? fmaf(2.f, om - c0, -d) : 0.f;
       srow[B][lane + HALO] = make_float4(sv, d, sv * sv, d * d);
     }
     if (hact) {
-      const double od = sizeof(TO) == 8 ? (double)o_h : (double)oh;
-      const float d = (float)__dsub_rn(ASYNC ? (double)oh : od, rh) * hmask;
-      const float sv = fmaf(2.f, oh - c0, -d) * hmask;
+      const double od = (sizeof(TO) == 8 && !ASYNC) ? (double)o_h : (double)oh;
+      const float d = himg ? (float)__dsub_rn(od, rh) : 0.f;
+      const float sv = himg ? fmaf(2.f, oh - c0, -d) : 0.f;
       srow[B][pin_h] = make_float4(sv, d, sv * sv, d * d);
     }
-    __syncwarp();
-    float hs = 0.f, hd = 0.f, hss = 0.f, hdd = 0.f;
-#pragma unroll
-    for (int k = 0; k < kSsimTaps; ++k) {
-      const float4 v = srow[B][lane + k];
-      const float wt = gtap(k < kSsimRadius ? kSsimRadius - k : k - kSsimRadius);
-      hs = fmaf(wt, v.x, hs);
-      hd = fmaf(wt, v.y, hd);
-      hss = fmaf(wt, v.z, hss);
-      hdd = fmaf(wt, v.w, hdd);
+    // software pipeline: filter row y-1 (converted last iteration) while the
+    // conversion of row y above is still in flight
+    if (y >= 1) {
+      constexpr int UP = (U + 10) % 11;  // (y-1) mod 11
+      filter_row(B ^ 1, y - 1, std::integral_constant<int, UP>{});
     }
-    float os, odv, oss, odd;
-    ring_step<U>(ring, hs, hd, hss, hdd, os, odv, oss, odd);
-    if (y >= 2 * kSsimRadius && col_valid) ssum += ssim_px(os, odv, oss, odd, c0, C1, C2);
+    __syncwarp();
     if constexpr (!ASYNC) {
       o_m = o_mn;
       o_h = o_hn;
@@ -260,19 +290,26 @@ k_eval_ssim(const EvalArgs args, const PcaParams inv) {
     }
   };
 
-  // 11-row blocks keep the ring slots static. The row buffer alternates with
-  // U's parity; rows 10 and 11 (= U 10 and U 0 of the next block) share
-  // parity 0, so a __syncwarp before the next block's first write separates
-  // the previous row's reads from it.
-  for (int64_t jb = 0; jb < H; jb += 11) {
+  // 11-row blocks keep the ring slots static (U = y mod 11).
+  for (int jb = 0; jb < H32; jb += 11) {
 #define CV_ROW(U)                                                   \
-  if (jb + U < H) do_row(jb + U, std::integral_constant<int, U>{});
+  if (jb + U < H32) do_row(jb + U, std::integral_constant<int, U>{});
     CV_ROW(0) CV_ROW(1) CV_ROW(2) CV_ROW(3) CV_ROW(4) CV_ROW(5)
     CV_ROW(6) CV_ROW(7) CV_ROW(8) CV_ROW(9) CV_ROW(10)
 #undef CV_ROW
-    __syncwarp();
     ssum_d += (double)ssum;  // float partials over at most 11 rows
     ssum = 0.f;
+  }
+  {  // drain: filter the last row
+    const int yl = H32 - 1;
+    switch (yl % 11) {
+#define CV_LAST(U) \
+  case U: filter_row(yl & 1, yl, std::integral_constant<int, U>{}); break;
+      CV_LAST(0) CV_LAST(1) CV_LAST(2) CV_LAST(3) CV_LAST(4) CV_LAST(5)
+      CV_LAST(6) CV_LAST(7) CV_LAST(8) CV_LAST(9) CV_LAST(10)
+#undef CV_LAST
+    }
+    ssum_d += (double)ssum;
   }
   if constexpr (ASYNC) cp_async_wait<0>();
   if constexpr (FRAMES) flag_warp(args.err, qmax > args.Li, CV_FLAG_INT_RANGE);

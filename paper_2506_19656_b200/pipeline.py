@@ -113,6 +113,31 @@ class Encoded:
             raise ConfigurationError("integer values outside the bit-depth range")
 
 
+class Workspace:
+    """Reusable device buffers for repeated calls on same-shaped cubes (frames,
+    filled cube, carry map, recon). Large allocations inside a hot loop make
+    the caching allocator fall back to cudaMalloc/cudaFree (which synchronise
+    the device) whenever fragmentation forbids a cached fit; a Workspace pins
+    them once. Buffers handed out for one call are overwritten by the next."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, name: str, shape, dtype, device) -> torch.Tensor:
+        key = (name, tuple(shape), dtype, str(device))
+        t = self._bufs.get(key)
+        if t is None:
+            t = torch.empty(tuple(shape), dtype=dtype, device=device)
+            self._bufs[key] = t
+        return t
+
+
+def _alloc(ws: Workspace | None, name, shape, dtype, device) -> torch.Tensor:
+    if ws is None:
+        return torch.empty(tuple(shape), dtype=dtype, device=device)
+    return ws.get(name, shape, dtype, device)
+
+
 def _as_batch(cube) -> tuple[dev.Arr, tuple]:
     x = dev.to_device(cube)
     if len(x.shape) == 4:
@@ -172,7 +197,7 @@ def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normaliz
 
 
 def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | None = None,
-                shard=None) -> Encoded:
+                shard=None, workspace: Workspace | None = None) -> Encoded:
     """Cube(s) -> planar integer frames + QuantParams (+ PCA models).
 
     Float32 cubes are forward-filled on the fly; the quantiser also writes the
@@ -197,7 +222,7 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
         seg_last = None
         if fill:
             nseg = lib.cv_num_segments(T, seg)
-            seg_last = torch.empty((B, nseg, HW * C), dtype=torch.float32, device=d)
+            seg_last = _alloc(workspace, "seg_last", (B, nseg, HW * C), torch.float32, d)
         if not sharded:
             qmins, qmaxs, nans = band_stats(x, B, T, HW * C, C, fill_mode=int(fill), seg_len=seg,
                                             fill_value=spec.fill_value, err=err, seg_last=seg_last)
@@ -238,10 +263,11 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
     groups = pack_groups(E)
     G = len(groups)
     tdt, _ = dev.out_dtype_for_depth(spec.bit_depth)
-    frames = torch.empty((B, G, T, 3, HW), dtype=tdt, device=d)
+    frames = _alloc(workspace, "frames", (B, G, T, 3, HW), tdt, d)
     filled = None
     if spec.n_pcs == 0 and fill:
-        filled = filled_out if filled_out is not None else torch.empty_like(x.t)
+        filled = filled_out if filled_out is not None else _alloc(workspace, "filled", x.t.shape,
+                                                                  x.t.dtype, d)
     for b in range(B) if spec.n_pcs else [None]:
         if b is None:
             _lib.call("cv_quantize", x.ptr, x.code, B, T, HW, C, qmins.data_ptr(), qmaxs.data_ptr(),
@@ -390,6 +416,7 @@ class HostStreamer:
         self.free = [torch.cuda.Event() for _ in range(2)]
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        self.ws = [Workspace(), Workspace()]
 
     def run(self, host: torch.Tensor) -> list:
         """host: pinned [B,T,H,W,C]; returns one metric report per cube."""
@@ -419,7 +446,7 @@ class HostStreamer:
                 issue(i + 1)
             comp.wait_event(self.ready[k])
             x = self.bufs[k][:n]
-            enc = encode_prep(x, self.spec)
+            enc = encode_prep(x, self.spec, workspace=self.ws[k])
             _, scores = decode_eval(enc, x, want_ssim=self.want_ssim, recon_out=self.recon[:n])
             self.free[k].record(comp)
             sse.append(scores.sse)
