@@ -242,6 +242,20 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins,
             int32_t want_ssim, float *recon_out, void *ws, double *sse,
             double *ssim_sum, uint32_t *err_word, void *stream);
 
+/* ---------------------------------------------------------------------- */
+/* spectral angle                           */
+/* ---------------------------------------------------------------------- */
+
+size_t cv_angle_ws_bytes(void);
+/*
+ * Per pixel theta = arccos(<o, r> / (|o| |r|)) over the C channels (float64),
+ * orig/recon channel-last [n_pix][C]. out (device, 3 doubles): sum of theta in
+ * degrees over pixels with non-zero norms, their count, the skipped count.
+ */
+int cv_spectral_angle(const void *orig, int32_t odtype, const void *recon,
+                      int32_t rdtype, int64_t n_pix, int32_t C, void *ws,
+                      double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,37 @@ def ssim(orig, recon, win: int = 11, sigma: float = 1.5) -> float:
     return float(ssim_per_band(orig, recon, win, sigma).mean())
 
 
+def spectral_angle(orig, recon):
+    """SPEC.md:437-445 — mean over pixels of arccos(<o,r>/(|o||r|)) in degrees;
+    zero-norm pixels skipped. Returns (mean_degrees, skipped)."""
+    o = np.asarray(orig, dtype=np.float64).reshape(-1, np.shape(orig)[-1])
+    r = np.asarray(recon, dtype=np.float64).reshape(-1, np.shape(recon)[-1])
+    no = np.sqrt((o * o).sum(axis=1))
+    nr = np.sqrt((r * r).sum(axis=1))
+    ok = (no > 0) & (nr > 0)
+    cs = np.clip((o[ok] * r[ok]).sum(axis=1) / (no[ok] * nr[ok]), -1.0, 1.0)
+    ang = np.degrees(np.arccos(cs))
+    return (float(ang.mean()) if ang.size else math.nan), int((~ok).sum())
+
+
+def spectral_angle_brute(orig, recon):
+    o = np.asarray(orig, dtype=np.float64)
+    r = np.asarray(recon, dtype=np.float64)
+    c = o.shape[-1]
+    o2, r2 = o.reshape(-1, c), r.reshape(-1, c)
+    tot, n, skip = 0.0, 0, 0
+    for i in range(o2.shape[0]):
+        dot = sum(o2[i, k] * r2[i, k] for k in range(c))
+        no = math.sqrt(sum(o2[i, k] ** 2 for k in range(c)))
+        nr = math.sqrt(sum(r2[i, k] ** 2 for k in range(c)))
+        if no == 0 or nr == 0:
+            skip += 1
+            continue
+        tot += math.degrees(math.acos(max(-1.0, min(1.0, dot / (no * nr)))))
+        n += 1
+    return (tot / n if n else math.nan), skip
+
+
 # --------------------------------------------------------------------------- brute force
 
 def psnr_brute(orig, recon):

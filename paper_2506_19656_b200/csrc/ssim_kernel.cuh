@@ -46,8 +46,12 @@ struct SsimShared {
 // ASYNC: f32 original + non-PCA u8/u16 frames with W a multiple of 4 (frame
 // rows then start 4-byte aligned): raw rows stream through the cp.async ring.
 // Otherwise: one-row register prefetch (PCA, f64/u16 originals, recon_in).
+#ifndef CVB_SSIM_MINB
+#define CVB_SSIM_MINB 2
+#endif
+
 template <typename TO, int RS, bool PCA, bool ASYNC>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, CVB_SSIM_MINB)
 k_eval_ssim(const EvalArgs args, const PcaParams inv) {
   using R = typename RawT<RS>::type;
   constexpr bool FRAMES = (RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16);

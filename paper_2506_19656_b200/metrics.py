@@ -125,6 +125,27 @@ def ssim(orig, recon) -> float:
     return float(np.mean(ssim_per_band(orig, recon)))
 
 
+def spectral_angle(orig, recon) -> tuple:
+    """Mean spectral angle in degrees over pixels and the
+    number of zero-norm pixels skipped: per pixel arccos(<o,r>/(|o||r|))."""
+    o, r = _prep_pair(orig, recon)
+    T, H, W, C = o.shape
+    d = o.device
+    n = T * H * W
+    out = torch.zeros(3, dtype=torch.float64, device=d)
+    if n:
+        lib = _lib.load()
+        ws = dev.workspace(lib.cv_angle_ws_bytes(), d)
+        _lib.call("cv_spectral_angle", o.ptr, o.code, r.ptr, r.code, n, C, ws.data_ptr(),
+                  out.data_ptr(), dev.stream_ptr(d))
+    s, cnt, skipped = out.cpu().tolist()
+    mean = s / cnt if cnt else float("nan")
+    if skipped:
+        warnings.warn(f"spectral angle: {int(skipped)} zero-norm pixels skipped", RuntimeWarning,
+                      stacklevel=2)
+    return mean, int(skipped)
+
+
 def evaluate(orig, recon, total_bytes: int | None = None, want_ssim: bool = True) -> dict:
     """psnr + ssim (+ bpppb) of one reconstruction, one fused device pass."""
     s = score(orig, recon, want_ssim=want_ssim)
@@ -134,6 +155,7 @@ def evaluate(orig, recon, total_bytes: int | None = None, want_ssim: bool = True
         per = s["ssim_sum"] / s["n_ssim_per_band"]
         rep["ssim_per_band"] = per
         rep["ssim"] = float(per.mean())
+    rep["sa_degrees"], rep["sa_skipped"] = spectral_angle(orig, recon)
     if total_bytes is not None:
         t, h, w, c = np.asarray(orig).shape if not isinstance(orig, torch.Tensor) else orig.shape
         rep["bpppb"] = bpppb(total_bytes, t, h, w, c)

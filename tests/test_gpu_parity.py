@@ -306,3 +306,17 @@ def test_batch_matches_single(cuda):
         assert torch.equal(encb.frames[b], enc1.frames[0])
         assert torch.equal(reconb[b], recon1)
         np.testing.assert_array_equal(scb.report()[b]["psnr_per_band"], sc1.report()[0]["psnr_per_band"])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_spectral_angle_vs_oracle(cuda, seed):
+    rng = np.random.default_rng(seed)
+    o = (rng.random((3, 10, 12, 5)) + 0.1).astype(np.float32)
+    r = o + 0.02 * rng.normal(size=o.shape)
+    o[0, 0, 0] = 0  # a zero-norm pixel, skipped
+    with pytest.warns(RuntimeWarning):
+        got, skipped = G_metrics.spectral_angle(o, r)
+    want, wskip = M.spectral_angle(o, r)
+    assert skipped == wskip == 1
+    assert abs(got - want) <= 1e-9 * want
+    assert G_metrics.spectral_angle(o[1:], o[1:])[0] < 1e-5

@@ -82,3 +82,29 @@ def test_gaussian_taps():
     np.testing.assert_allclose(g[5:], [0.26601172486179436, 0.2130055377112537, 0.10936068950970002,
                                       0.03600077212843083, 0.007598758135239185, 0.00102838008447911],
                                rtol=1e-12)
+
+
+def test_spectral_angle_known_answers():
+    o = np.array([1.0, 0.0]).reshape(1, 1, 1, 2)
+    assert abs(M.spectral_angle(o, np.array([0.0, 1.0]).reshape(1, 1, 1, 2))[0] - 90.0) < 1e-12
+    assert abs(M.spectral_angle(np.array([1.0, 1.0]).reshape(1, 1, 1, 2), o)[0] - 45.0) < 1e-12
+    rng = np.random.default_rng(4)
+    x = rng.random((2, 3, 4, 5)) + 0.1
+    assert M.spectral_angle(x, x)[0] < 1e-5
+    # invariant under per-pixel positive scaling
+    s = rng.random((2, 3, 4, 1)) + 0.5
+    np.testing.assert_allclose(M.spectral_angle(x, x * 1.1 + 0.01)[0],
+                               M.spectral_angle(x * s, (x * 1.1 + 0.01) * s)[0], rtol=1e-9)
+    z = x.copy()
+    z[0, 0, 0] = 0
+    assert M.spectral_angle(z, x)[1] == 1
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_spectral_angle_vs_brute(seed):
+    rng = np.random.default_rng(200 + seed)
+    o = rng.random((4, 8, 8, 3))
+    r = o + 0.05 * rng.normal(size=o.shape)
+    a, s = M.spectral_angle(o, r)
+    b, t = M.spectral_angle_brute(o, r)
+    assert s == t and abs(a - b) <= 1e-9 * abs(b)
