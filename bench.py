@@ -405,7 +405,9 @@ def run_ours(a):
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"config{a.config}", {}).get(dom)
+        ent = json.loads(prof.read_text()).get(f"config{a.config}", {}).get(dom)
+        if ent:  # ncu dram__bytes_read+write per element (profiles/) x elements per launch
+            traffic = ent["dram_bytes_per_elem"] * wl.elem_rank
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
