@@ -24,6 +24,9 @@
 
 #include "eval_kernel.cuh"
 #include "ssim_kernel.cuh"
+#include "ssim4_kernel.cuh"
+
+#include <cstdlib>
 
 namespace cvb {
 
@@ -66,6 +69,22 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
     const int ncg = (a.C + kSsimWarpsPerCta - 1) / kSsimWarpsPerCta;
     const int wpc = a.C < kSsimWarpsPerCta ? a.C : kSsimWarpsPerCta;
     dim3 grid((unsigned)(a.nstrips * ncg), (unsigned)a.T, (unsigned)n);
+    if constexpr ((RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) && std::is_same<TO, float>::value) {
+      if (!pca && a.W % 4 == 0 && !getenv("CVB_SSIM_V4")) {
+        const int ncg4 = (a.C + kS4Chans - 1) / kS4Chans;
+        const int ngrp = (int)((a.W + kS4Strips * kSsimStrip - 1) / (kS4Strips * kSsimStrip));
+        dim3 g4((unsigned)(ngrp * ncg4), (unsigned)a.T, (unsigned)n);
+        const size_t sm = sizeof(Ssim4Shared);
+        if (a.bit_depth <= 10) {
+          cudaFuncSetAttribute(k_eval_ssim4<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          k_eval_ssim4<RS, true><<<g4, 32 * kS4Strips * kS4Chans, sm, st>>>(a);
+        } else {
+          cudaFuncSetAttribute(k_eval_ssim4<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          k_eval_ssim4<RS, false><<<g4, 32 * kS4Strips * kS4Chans, sm, st>>>(a);
+        }
+        return check_launch("cv_eval(ssim4)");
+      }
+    }
     if constexpr (RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) {
       if (pca) k_eval_ssim<TO, RS, true, false><<<grid, 32 * wpc, 0, st>>>(a, inv);
       else if (std::is_same<TO, float>::value && a.W % 4 == 0)
