@@ -21,8 +21,19 @@ constexpr int kS4Chans = 2;
 constexpr int kS4Row = kS4Strips * kSsimStrip + 2 * kSsimRadius;  // 138
 constexpr int kS4LutMax = 1024;                                    // bit depth <= 10
 
+// Row-buffer entry: (s, d) with the squares formed by the filter (halves the
+// shared-memory bytes the 11-tap horizontal filter reads; the smem pipe is
+// the co-bottleneck of this kernel), or (s, d, s^2, d^2) with CVB_SROW_F4.
+#ifdef CVB_SROW_F4
+using SRow = float4;
+__device__ __forceinline__ SRow make_srow(float s, float d) { return make_float4(s, d, s * s, d * d); }
+#else
+using SRow = float2;
+__device__ __forceinline__ SRow make_srow(float s, float d) { return make_float2(s, d); }
+#endif
+
 struct Ssim4Shared {
-  float4 srow[kS4Chans][2][kS4Row];
+  SRow srow[kS4Chans][2][kS4Row];
   float raw_o[kS4Strips * kS4Chans][kStages][40];       // 32 main + 5 halo (+pad)
   uint32_t raw_f[kS4Strips * kS4Chans][kStages][24];    // 48 samples (u16 pairs / u8 quads)
   double lut[kS4Chans][kS4LutMax];
@@ -79,7 +90,7 @@ k_eval_ssim4(const EvalArgs args) {
   for (int i = threadIdx.x; i < kS4Chans * 2 * kS4Row; i += blockDim.x) {
     const int e = i % kS4Row;
     const int64_t x = x0c - HALO + e;
-    if (x < 0 || x >= W) (&sh.srow[0][0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (x < 0 || x >= W) (&sh.srow[0][0][0])[i] = make_srow(0.f, 0.f);
   }
   __syncthreads();
   if (!chan_ok || j >= nvalid) return;  // absent strip / band: no barrier use below
@@ -146,7 +157,7 @@ k_eval_ssim4(const EvalArgs args) {
   const bool wr = args.recon_out != nullptr && mimg;
   float *wq = (args.recon_out ? args.recon_out : reinterpret_cast<float *>(0)) + (a * T + t) * inner +
               (mimg ? xm : 0) * C + c;
-  float4(*srow)[kS4Row] = sh.srow[cl];
+  SRow(*srow)[kS4Row] = sh.srow[cl];
   double sse = 0.0, ssum_d = 0.0;
   float ssum = 0.f;
   Ring ring;
@@ -162,16 +173,21 @@ k_eval_ssim4(const EvalArgs args) {
 
   auto filter_row = [&](int b, int y, auto ucst) {
     constexpr int U = decltype(ucst)::value;
-    const float4 *sr = &srow[b][j * kSsimStrip + lane];
+    const SRow *sr = &srow[b][j * kSsimStrip + lane];
     float hs = 0.f, hd = 0.f, hss = 0.f, hdd = 0.f;
 #pragma unroll
     for (int k = 0; k < kSsimTaps; ++k) {
-      const float4 v = sr[k];
+      const SRow v = sr[k];
       const float wt = gtap(k < kSsimRadius ? kSsimRadius - k : k - kSsimRadius);
       hs = fmaf(wt, v.x, hs);
       hd = fmaf(wt, v.y, hd);
+#ifdef CVB_SROW_F4
       hss = fmaf(wt, v.z, hss);
       hdd = fmaf(wt, v.w, hdd);
+#else
+      hss = fmaf(wt * v.x, v.x, hss);
+      hdd = fmaf(wt * v.y, v.y, hdd);
+#endif
     }
     float os, odv, oss, odd;
     ring_step<U>(ring, hs, hd, hss, hdd, os, odv, oss, odd);
@@ -194,7 +210,7 @@ k_eval_ssim4(const EvalArgs args) {
       if (wr) *wq = (float)rm;
       const float d = (float)diff;
       const float sv = fmaf(2.f, om - c0, -d);
-      srow[b][sidx_m] = make_float4(sv, d, sv * sv, d * d);
+      srow[b][sidx_m] = make_srow(sv, d);
     }
     wq += rowlen;
     if (himg) {
@@ -202,7 +218,7 @@ k_eval_ssim4(const EvalArgs args) {
       const double rh = recon(frame_at(s, fi_h));
       const float d = (float)__dsub_rn((double)oh, rh);
       const float sv = fmaf(2.f, oh - c0, -d);
-      srow[b][sidx_h] = make_float4(sv, d, sv * sv, d * d);
+      srow[b][sidx_h] = make_srow(sv, d);
     }
     if (y >= 1) filter_row(b ^ 1, y - 1, std::integral_constant<int, (U + 10) % 11>{});
     named_bar(bar_id, bar_n);  // row y complete for all strips of the band
