@@ -25,6 +25,7 @@
 #include "eval_kernel.cuh"
 #include "ssim_kernel.cuh"
 #include "ssim4_kernel.cuh"
+#include "ssim6_kernel.cuh"
 
 #include <cstdlib>
 
@@ -70,6 +71,19 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
     const int wpc = a.C < kSsimWarpsPerCta ? a.C : kSsimWarpsPerCta;
     dim3 grid((unsigned)(a.nstrips * ncg), (unsigned)a.T, (unsigned)n);
     if constexpr ((RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) && std::is_same<TO, float>::value) {
+      if (a.ssim6) {
+        const int ncg6 = (a.C + k6Chans - 1) / k6Chans;
+        dim3 g6((unsigned)(ssim6_groups(a.W) * ncg6), (unsigned)a.T, (unsigned)n);
+        const size_t sm = sizeof(Ssim6Shared);
+        if (a.bit_depth <= 10) {
+          cudaFuncSetAttribute(k_eval_ssim6<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          k_eval_ssim6<RS, true><<<g6, 32 * 4 * k6Chans, sm, st>>>(a);
+        } else {
+          cudaFuncSetAttribute(k_eval_ssim6<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          k_eval_ssim6<RS, false><<<g6, 32 * 4 * k6Chans, sm, st>>>(a);
+        }
+        return check_launch("cv_eval(ssim6)");
+      }
       if (!pca && a.W % 4 == 0 && !getenv("CVB_SSIM_V4")) {
         const int ncg4 = (a.C + kS4Chans - 1) / kS4Chans;
         const int ngrp = (int)((a.W + kS4Strips * kSsimStrip - 1) / (kS4Strips * kSsimStrip));
@@ -136,7 +150,8 @@ size_t cv_eval_ws_bytes(int64_t n_cubes, int64_t T, int64_t H, int64_t W, int32_
   (void)H;
   if (C <= 0) return 0;
   const int TX = eval_tx(C, want_ssim != 0);
-  const int64_t nstrips = (W + TX - 1) / TX;
+  int64_t nstrips = (W + TX - 1) / TX;
+  if (want_ssim && W >= kSsimTaps && 4 * (int64_t)ssim6_groups(W) > nstrips) nstrips = 4 * (int64_t)ssim6_groups(W);
   return (size_t)(n_cubes * T * nstrips * 2 * C) * sizeof(double);
 }
 
@@ -202,6 +217,9 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, 
   const bool ssim = want_ssim != 0;
   a.TX = eval_tx(C, ssim);
   a.nstrips = (int)((W + a.TX - 1) / a.TX);
+  // vertical-first SSIM kernel: frames, float32 original, no PCA, 4-byte aligned frame rows
+  a.ssim6 = ssim && frames && !pca && odtype == CV_F32 && W % 4 == 0 && !getenv("CVB_SSIM_V5");
+  if (a.ssim6) a.nstrips = 4 * ssim6_groups(W);
   cudaStream_t st = (cudaStream_t)stream;
   int s;
   switch (odtype) {

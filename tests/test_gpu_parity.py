@@ -320,3 +320,23 @@ def test_spectral_angle_vs_oracle(cuda, seed):
     assert skipped == wskip == 1
     assert abs(got - want) <= 1e-9 * want
     assert G_metrics.spectral_angle(o[1:], o[1:])[0] < 1e-5
+
+
+@pytest.mark.parametrize("shape,B", [((3, 11, 12, 2), 8), ((2, 37, 260, 3), 10), ((2, 20, 244, 5), 16),
+                                     ((1, 130, 128, 7), 12), ((2, 16, 124, 1), 8), ((1, 12, 468, 4), 10)])
+def test_ssim_column_groups(cuda, shape, B):
+    """The vertical-first SSIM kernel (W % 4 == 0): CTAs of 116 output columns
+    overlapping by 12 input columns, odd row counts, 8-bit (u8 frames) to
+    16-bit, with and without the dequantisation table; SSE and recon writes
+    counted once per element."""
+    rng = np.random.default_rng(sum(shape) + B)
+    x = (rng.random(shape) * 2 + 0.5).astype(np.float32)
+    x[rng.random(shape) < 0.05] = np.nan
+    enc, recon, sc = G_pipe.roundtrip(torch.from_numpy(x).to(cuda), G_pipe.StreamSpec(B))
+    enc.check()
+    ref = O.encode_stream(x, B)
+    rec_o = O.decode_stream(ref["frames"], ref, x.shape, B)
+    np.testing.assert_array_equal(recon.cpu().numpy(), rec_o.astype(np.float32))
+    rep = sc.report()[0]
+    np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), rtol=1e-9)
+    np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
