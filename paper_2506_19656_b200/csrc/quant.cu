@@ -15,6 +15,9 @@
 // segment's first carry comes from the per-segment last-observed map. Planar
 // output is staged in shared memory and written as 16-byte vectors per plane.
 #include "common.cuh"
+
+#include <cstdlib>
+#include <type_traits>
 #include "pca_params.cuh"
 
 namespace cvb {
@@ -375,22 +378,33 @@ template <typename TIn, typename TOut, bool FILL, bool PCA>
 static int launch_qp(const void *src, void *out, const QuantArgs &args, const PcaParams &pca,
                      int64_t n_cubes, cudaStream_t st) {
   constexpr int VE = 16 / sizeof(TIn);
-  const int NT = 256;
-  const int NE = NT * args.C;
+  // pixel pairs with register-resident band constants (the common case)
+  const bool px2 = !PCA && args.C <= kQRegC && args.HW % 2 == 0 && !getenv("CVB_QP_PX1");
+  const int NT = px2 ? 128 : 256;
+  const int P = px2 ? 2 * NT : NT;
+  const int NE = P * args.C;
   const int SP = (NE + VE - 1) / VE * VE;
   const size_t sm = (size_t)kQStages * SP * sizeof(TIn) + kMaxC * (sizeof(QBand) + sizeof(QBand32));
-  dim3 grid((unsigned)((args.HW + NT - 1) / NT), (unsigned)cv_num_segments(args.T, args.seg_len),
+  dim3 grid((unsigned)((args.HW + P - 1) / P), (unsigned)cv_num_segments(args.T, args.seg_len),
             (unsigned)n_cubes);
-  const int mv = (args.C + VE - 1) / VE;  // vectors per thread per step
-#define CV_QP(MV)                                                                                     \
+  const int mv = (P / NT * args.C + VE - 1) / VE;  // vectors per thread per step
+#define CV_QP(MV, X2)                                                                                 \
   do {                                                                                                \
-    auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, MV>;                                          \
+    auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, MV, X2>;                                      \
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
   } while (0)
-  if (mv <= 2) CV_QP(2);
-  else if (mv <= 4) CV_QP(4);
-  else CV_QP(8);
+  if constexpr (!PCA) {
+    if (px2) {
+      if (mv <= 2) CV_QP(2, true);
+      else if (mv <= 4) CV_QP(4, true);
+      else CV_QP(8, true);
+      return check_launch("cv_quantize(planar)");
+    }
+  }
+  if (mv <= 2) CV_QP(2, false);
+  else if (mv <= 4) CV_QP(4, false);
+  else CV_QP(8, false);
 #undef CV_QP
   return check_launch("cv_quantize(planar)");
 }

@@ -29,7 +29,12 @@ __device__ __forceinline__ void cp_async_wait_q() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV>
+// PX2 (non-PCA, C <= kQRegC, even H*W): thread p takes the pixel pair 2p,
+// 2p+1, keeps every band's float32 quantiser constants in registers and
+// stores both samples of a plane with one 32-bit (u16) / 16-bit (u8) store.
+constexpr int kQRegC = 8;
+
+template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false>
 __global__ void __launch_bounds__(256)
 k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs args,
                   const PcaParams pca) {
@@ -38,7 +43,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   const int NT = blockDim.x, tid = threadIdx.x;
   const int C = args.C, E = args.E;
   const int64_t T = args.T, HW = args.HW, inner = HW * C;
-  const int P = NT;
+  const int P = PX2 ? 2 * NT : NT;          // pixels per chunk
   const int NE = P * C;                     // elements per full chunk
   const int64_t a = blockIdx.z, seg = blockIdx.y, nseg = gridDim.y;
   const int64_t pix0 = (int64_t)blockIdx.x * P;
@@ -91,10 +96,17 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   }
 
   // per-pixel constants
-  const int p = tid;
+  const int p = PX2 ? 2 * tid : tid;
   const bool pvalid = p < npix;
   bool bad = false, nanbad = false;
   TOut *obase = out + (a * args.G * T) * 3 * HW + pix0 + p;
+  QBand32 rb[PX2 ? kQRegC : 1];
+  const int64_t gjump = (3 * T - 2) * HW;  // plane 2 of video g -> plane 0 of video g+1
+  if constexpr (PX2) obase += t0 * 3 * HW;
+  if constexpr (PX2) {
+#pragma unroll
+    for (int c = 0; c < kQRegC; ++c) rb[c] = qtab32[c < C ? c : 0];
+  }
 
   for (int64_t t = t0; t < t1; ++t) {
     cp_async_wait_q<kQStages - 2>();
@@ -123,7 +135,40 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
     // refill the stage consumed one step ago (every thread is past it now)
     if (t + kQStages - 1 < t1) issue(t + kQStages - 1);
     cp_async_commit_q();
-    if (pvalid) {
+    if (PX2 && pvalid) {
+      // pixel pair (p, p+1); npix and p are even
+      const TIn *px = st + p * C;
+      TOut *op = obase + (t - t0) * 3 * HW;  // plane 0 of video 0 at time t
+      using W2 = typename std::conditional<sizeof(TOut) == 1, uint16_t, uint32_t>::type;
+      uint32_t l0 = 0, l1 = 0;
+#pragma unroll
+      for (int pl = 0; pl < 3 * ((kQRegC + 2) / 3); ++pl) {
+        if (pl < 3 * args.G) {
+          const int c = pl;
+          uint32_t q0, q1;
+          if (c < C) {
+            const float v0 = (float)px[c], v1 = (float)px[C + c];
+            if constexpr (!FILL) nanbad |= (v0 != v0) | (v1 != v1);
+            const QBand32 b32 = rb[c];
+            const bool f0 = b32.use32 && quantize_fast32(v0, b32, q0, bad);
+            const bool f1 = b32.use32 && quantize_fast32(v1, b32, q1, bad);
+            if (!(f0 && f1)) {
+              const QBand b = qtab[c];
+              if (!f0) q0 = quantize_value(range_prep((double)v0, b, args.clamp, bad), b);
+              if (!f1) q1 = quantize_value(range_prep((double)v1, b, args.clamp, bad), b);
+            }
+            l0 = q0;
+            l1 = q1;
+          } else {
+            const bool rep = args.pad_mode == CV_PAD_REPEAT;
+            q0 = rep ? l0 : 0u;
+            q1 = rep ? l1 : 0u;
+          }
+          *reinterpret_cast<W2 *>(op) = (W2)(q0 | (q1 << (8 * sizeof(TOut))));
+          op += (pl % 3 == 2) ? gjump : HW;  // next plane / next video
+        }
+      }
+    } else if (!PX2 && pvalid) {
       const TIn *px = st + p * C;
       TOut *o = obase + t * 3 * HW;
       if constexpr (!PCA) {

@@ -138,11 +138,22 @@ k_stats_vec(const TIn *__restrict__ src, int64_t T, int64_t inner, int C, int fi
 #pragma unroll
     for (int k = 0; k < KV; ++k) last[k][j] = __int_as_float(0x7fc00000);
   }
-  bool inf_seen = false;
   V cur[KV], nxt[KV];
 #pragma unroll
   for (int k = 0; k < KV; ++k)
     if (vok[k] && t0 < t1) cur[k] = __ldg(reinterpret_cast<const V *>(cube + t0 * inner + voff[k]));
+  // leading gap flag: NaN in the cube's first frame
+  if (t0 == 0 && t0 < t1) {
+#pragma unroll
+    for (int k = 0; k < KV; ++k)
+      if (vok[k]) {
+        const float x[VEC] = {(float)cur[k].x, (float)cur[k].y, (float)cur[k].z, (float)cur[k].w};
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) lead[j] |= isnan(x[j]);
+      }
+  }
+  // per element: min/max (fminf/fmaxf skip NaN; an infinity ends up as the
+  // band's min or max and is flagged below), NaN count, last observation
   for (int64_t t = t0; t < t1; ++t) {
     if (t + 1 < t1) {
 #pragma unroll
@@ -155,20 +166,22 @@ k_stats_vec(const TIn *__restrict__ src, int64_t T, int64_t inner, int C, int fi
       const float x[VEC] = {(float)cur[k].x, (float)cur[k].y, (float)cur[k].z, (float)cur[k].w};
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        // fminf/fmaxf skip NaN; infinities are flagged and kept out of the range
-        const bool nan = isnan(x[j]);
-        const bool inf = isinf(x[j]);
-        inf_seen |= inf;
-        const float v = inf ? mn[j] : x[j];
-        mn[j] = fminf(mn[j], v);
-        mx[j] = fmaxf(mx[j], inf ? mx[j] : x[j]);
+        const bool nan = x[j] != x[j];
+        mn[j] = fminf(mn[j], x[j]);
+        mx[j] = fmaxf(mx[j], x[j]);
         nanc[j] += nan ? 1u : 0u;
-        lead[j] |= nan && (t == 0);
-        if (!nan && !inf) last[k][j] = x[j];
+        last[k][j] = nan ? last[k][j] : x[j];
       }
     }
 #pragma unroll
     for (int k = 0; k < KV; ++k) cur[k] = nxt[k];
+  }
+  bool inf_seen = false;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    // an infinity is the band's extreme once seen (the initial +/-INF of an
+    // empty range sit on the opposite sides); it is an error either way
+    inf_seen |= (mn[j] == -INFINITY) || (mx[j] == INFINITY);
   }
   if (seg_last && t0 < t1) {
     float *sl = seg_last + (a * nseg + seg) * inner;

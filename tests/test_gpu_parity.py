@@ -323,12 +323,15 @@ def test_spectral_angle_vs_oracle(cuda, seed):
 
 
 @pytest.mark.parametrize("shape,B", [((3, 11, 12, 2), 8), ((2, 37, 260, 3), 10), ((2, 20, 244, 5), 16),
-                                     ((1, 130, 128, 7), 12), ((2, 16, 124, 1), 8), ((1, 12, 468, 4), 10)])
+                                     ((1, 130, 128, 7), 12), ((2, 16, 124, 1), 8), ((1, 12, 468, 4), 10),
+                                     # 16-byte aligned rows: bulk-copy input path
+                                     ((2, 24, 248, 3), 10), ((1, 16, 376, 5), 16), ((2, 40, 128, 8), 8),
+                                     ((1, 13, 256, 7), 10), ((2, 11, 16, 2), 12)])
 def test_ssim_column_groups(cuda, shape, B):
-    """The vertical-first SSIM kernel (W % 4 == 0): CTAs of 116 output columns
-    overlapping by 12 input columns, odd row counts, 8-bit (u8 frames) to
-    16-bit, with and without the dequantisation table; SSE and recon writes
-    counted once per element."""
+    """The vertical-first SSIM kernel (W % 4 == 0): CTAs of 118 output columns
+    overlapping by 10 input columns, odd row counts, 8-bit (u8 frames) to
+    16-bit, with and without the dequantisation table, per-lane and bulk-copy
+    input paths; SSE and recon writes counted once per element."""
     rng = np.random.default_rng(sum(shape) + B)
     x = (rng.random(shape) * 2 + 0.5).astype(np.float32)
     x[rng.random(shape) < 0.05] = np.nan
