@@ -148,6 +148,10 @@ k_eval_ssim6(const EvalArgs args) {
   }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
+  // every ring slot starts out free: complete phase 0 of its `empty` barrier
+  if (threadIdx.x < k6Chans * k6Ring) mbar_arrive(&sh.empty[0][0] + threadIdx.x);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
   if (c >= C) return;  // absent band: its four warps leave together
 
   const double peak = args.peaks[a * C + c];
@@ -180,6 +184,14 @@ k_eval_ssim6(const EvalArgs args) {
   constexpr uint32_t kPO = 32 * sizeof(float), kPF = 16 * sizeof(uint32_t);
   const int H32 = (int)H;
   // copy row yi into stage yi % k6Stages (rows past the frame: empty group)
+  auto issue_s = [&](auto scst) {  // steady state: the row exists, stage S static
+    constexpr uint32_t S = decltype(scst)::value;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_o + S * kPO), "l"(ip_o) : "memory");
+    if (fok) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + S * kPF), "l"(ip_f) : "memory");
+    ip_o += ostride;
+    ip_f += fstride;
+    cp_async_commit();
+  };
   auto issue = [&](int yi) {
     if (yi < H32) {
       const uint32_t s = (uint32_t)yi & (k6Stages - 1);
@@ -202,8 +214,7 @@ k_eval_ssim6(const EvalArgs args) {
   float ssum = 0.f;
 
   // convert row y (stage y % k6Stages) into (s, d); SSE + recon write
-  auto convert = [&](int y, float &sv, float &dv) {
-    const int st = y & (k6Stages - 1);
+  auto convert = [&](int st, float &sv, float &dv) {
     const float om = sh.raw_o[w][st][lane];
     const uint32_t q = (sh.raw_f[w][st][fw] >> fsh) & ((1u << (32 / FPW)) - 1u);
     double rm;
@@ -230,7 +241,7 @@ k_eval_ssim6(const EvalArgs args) {
   float sv_n, dv_n;
   cp_async_wait<k6Depth - 1>();
   __syncwarp();
-  convert(0, sv_n, dv_n);
+  convert(0, sv_n, dv_n);  // stage 0
 
   // mbarrier pipeline: every warp stores column-filtered row e into ring slot
   // e % 8 (after the slot's previous row was filtered: empty barrier) and
@@ -246,6 +257,7 @@ k_eval_ssim6(const EvalArgs args) {
   auto consume = [&](int e) {
     const int slot = e & (k6Ring - 1);
     mbar_wait(&sh.full[cl][slot], (uint32_t)(e >> 3) & 1u);
+    __syncwarp();
     const float4 *hv = &sh.vb[cl][slot][0][hq];
     float4 acc[4];
 #pragma unroll
@@ -269,36 +281,66 @@ k_eval_ssim6(const EvalArgs args) {
       ssum += hvalid[i] ? s0 : 0.f;
     }
   };
-  // input row y (P = y % 4): issue row y + k6Depth, convert row y + 1, FIR
-  // step of row y; from row 10 on store column-filtered row e = y - 10 and
-  // filter row e-1
-  auto do_row = [&](int y, auto pcst) {
-    constexpr int P = decltype(pcst)::value;
+  // input row y (generic: runtime bounds and indices): issue row y + k6Depth,
+  // convert row y + 1, FIR step of row y; from row 10 on store column-filtered
+  // row e = y - 10 and filter row e-1 (warp (e-1) % 4)
+  auto do_row = [&](int y) {
     const float sv = sv_n, dv = dv_n;
     issue(y + k6Depth);
     if (y + 1 < H32) {
       cp_async_wait<k6Depth - 1>();
       __syncwarp();
-      convert(y + 1, sv_n, dv_n);
+      convert((y + 1) & (k6Stages - 1), sv_n, dv_n);
     }
     const float4 o = fir4_step(fir, sv, dv);
     if (y >= 2 * kSsimRadius) {
       const int e = y - 2 * kSsimRadius;
       const int slot = e & (k6Ring - 1);
-      if (e >= k6Ring) mbar_wait(&sh.empty[cl][slot], (uint32_t)((e >> 3) + 1) & 1u);
+      mbar_wait(&sh.empty[cl][slot], (uint32_t)(e >> 3) & 1u);
       vbw[slot * kVbRow] = o;
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.full[cl][slot]);
-      // consumer of row e-1: warp (e-1) % 4 = (y + 1) % 4 = (P + 1) % 4
-      if (e >= 1 && j == ((P + 1) & 3)) consume(e - 1);
+      if (e >= 1 && j == ((e - 1) & 3)) consume(e - 1);
     }
   };
+  // steady state (P = y % 8 static; rows y+1 and y+k6Depth exist, y >= 16):
+  // stage, ring slot and consumer warp are compile-time, no bounds checks
+  auto do_row_s = [&](int y, auto pcst) {
+    constexpr int P = decltype(pcst)::value;
+    constexpr int SL = (P + 8 - 2 * kSsimRadius % 8) % 8;  // ring slot of e = y - 10
+    const float sv = sv_n, dv = dv_n;
+    issue_s(std::integral_constant<uint32_t, (P + k6Depth) % k6Stages>{});
+    cp_async_wait<k6Depth - 1>();
+    __syncwarp();
+    convert((P + 1) % k6Stages, sv_n, dv_n);
+    const float4 o = fir4_step(fir, sv, dv);
+    const int e = y - 2 * kSsimRadius;
+    mbar_wait(&sh.empty[cl][SL], (uint32_t)(e >> 3) & 1u);
+    vbw[SL * kVbRow] = o;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.full[cl][SL]);
+  };
+  // in a steady half-block of rows y..y+3 warp j filters the one row the
+  // per-row schedule gives it (position (j+3)%4: row y + (j+3)%4 - 11), once,
+  // after the four rows: the filter body exists twice in the loop, not 8x
+  const int pj = (j + 3) & 3;
 
-  for (int y = 0; y < H32; y += 4) {
-    do_row(y, std::integral_constant<int, 0>{});
-    if (y + 1 < H32) do_row(y + 1, std::integral_constant<int, 1>{});
-    if (y + 2 < H32) do_row(y + 2, std::integral_constant<int, 2>{});
-    if (y + 3 < H32) do_row(y + 3, std::integral_constant<int, 3>{});
+  static_assert(k6Stages == 8 && k6Ring == 8, "steady-state loop is unrolled by 8");
+  for (int y = 0; y < H32; y += 8) {
+    if (y >= 16 && y + 7 + k6Depth < H32) {
+      do_row_s(y, std::integral_constant<int, 0>{});
+      do_row_s(y + 1, std::integral_constant<int, 1>{});
+      do_row_s(y + 2, std::integral_constant<int, 2>{});
+      do_row_s(y + 3, std::integral_constant<int, 3>{});
+      consume(y + pj - 2 * kSsimRadius - 1);
+      do_row_s(y + 4, std::integral_constant<int, 4>{});
+      do_row_s(y + 5, std::integral_constant<int, 5>{});
+      do_row_s(y + 6, std::integral_constant<int, 6>{});
+      do_row_s(y + 7, std::integral_constant<int, 7>{});
+      consume(y + 4 + pj - 2 * kSsimRadius - 1);
+    } else {
+      for (int k = 0; k < 8 && y + k < H32; ++k) do_row(y + k);
+    }
     ssum_d += (double)ssum;
     ssum = 0.f;
   }

@@ -61,7 +61,7 @@ def main(tag, elements, config="config2"):
                 shutil.copy(g, OUT / f"{tag}_{k}_details.txt")
     (OUT / f"{tag}_ncu_summary.json").write_text(json.dumps(summary, indent=1))
     traffic_path.write_text(json.dumps(traffic, indent=1))
-    lf = src / "launches_r01.csv"
+    lf = src / f"launches_{tag}.csv"
     if lf.exists():
         shutil.copy(lf, OUT / f"{tag}_launches.csv")
     print(json.dumps({p: (round(m["gpu__time_duration.sum"] * 1e3, 3), round(m["dram_bytes_per_elem"], 2),
