@@ -56,10 +56,25 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
   bool nonfinite = false, isn = false;
 
   const int64_t nchunks = (n_pix + P - 1) / P;
+  const int64_t ne = n_pix * C;
+  // register prefetch of the next chunk (the staging barrier no longer
+  // exposes the full load latency per chunk)
+  TIn nxt[kGramK];
+  auto fetch = [&](int64_t ch) {
+#pragma unroll
+    for (int k = 0; k < kGramK; ++k) {
+      const int64_t e = ch * P * C + tid + k * NT;
+      nxt[k] = (ch < nchunks && e < ne) ? ldg(src + e) : TIn(0);
+    }
+  };
+  fetch(blockIdx.x);
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t pix0 = ch * P;
     const int64_t e0 = pix0 * C;
-    const int64_t ne = n_pix * C;
+    TIn cur[kGramK];
+#pragma unroll
+    for (int k = 0; k < kGramK; ++k) cur[k] = nxt[k];
+    fetch(ch + gridDim.x);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kGramK; ++k) {
@@ -67,7 +82,7 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
       const int64_t e = e0 + el;
       double d = 0.0;
       if (e < ne) {
-        const TIn v = ldg(src + e);
+        const TIn v = cur[k];
         const double vd = (double)v;
         if constexpr (is_float_t<TIn>::value) {
           if (isnan(v)) isn = true;
@@ -229,6 +244,78 @@ k_pca_project(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
   }
 }
 
+// Projection for C <= CM: one thread per pixel, its C values loaded straight
+// into registers (a warp reads 32*C contiguous values), the differences to
+// the mean kept in registers (CM static) and the K <= KB components formed
+// with constant-bank weights; per-component min/max in registers. Several
+// pixels per thread are in flight (PPT) to cover the load latency.
+template <typename TIn, typename TO, int KB, int CM, int PPT>
+__global__ void __launch_bounds__(256)
+k_pca_project_px(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
+                 StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err) {
+  const int C = pca.C, K = pca.K;
+  const int64_t a = blockIdx.y;
+  const TIn *cube = src + a * n_pix * C;
+  double mn[KB], mx[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    mn[j] = INFINITY;
+    mx[j] = -INFINITY;
+  }
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * PPT;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x * PPT + threadIdx.x; p0 < n_pix; p0 += stride) {
+    TIn v[PPT][CM];
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const int64_t pix = p0 + (int64_t)u * blockDim.x;
+#pragma unroll
+      for (int c = 0; c < CM; ++c) v[u][c] = (c < C && pix < n_pix) ? ldg(cube + pix * C + c) : TIn(0);
+    }
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const int64_t pix = p0 + (int64_t)u * blockDim.x;
+      if (pix >= n_pix) break;
+      double d[CM];
+#pragma unroll
+      for (int c = 0; c < CM; ++c) {
+        const double x = (double)v[u][c];
+        if (c < C) bad |= !isfinite(x);
+        d[c] = c < C ? __dsub_rn(x, pca.mean[c]) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        if (j < K) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < CM; ++c)
+            if (c < C) acc = __fma_rn(d[c], pca.W[j * kMaxC + c], acc);
+          mn[j] = fmin(mn[j], acc);
+          mx[j] = fmax(mx[j], acc);
+          if (out) out[(a * n_pix + pix) * K + j] = (TO)acc;
+        }
+      }
+    }
+  }
+  flag_warp(err, bad, CV_FLAG_NONFINITE);
+  if (stats) {
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      if (j < K) {
+        double a_mn = mn[j], a_mx = mx[j];
+        for (int o = 16; o > 0; o >>= 1) {
+          a_mn = fmin(a_mn, __shfl_xor_sync(0xffffffffu, a_mn, o));
+          a_mx = fmax(a_mx, __shfl_xor_sync(0xffffffffu, a_mx, o));
+        }
+        if ((threadIdx.x & 31) == 0 && a_mn <= a_mx) {
+          atomicMin(&stats[a * K + j].min_key, dkey(a_mn));
+          atomicMax(&stats[a * K + j].max_key, dkey(a_mx));
+        }
+      }
+    }
+  }
+}
+
 // Inverse projection: one thread per pixel.
 template <typename TIn, typename TO>
 __global__ void __launch_bounds__(256)
@@ -266,7 +353,7 @@ static int gram_blocks(int64_t n_pix, int C) {
   const int NT = threads_for_channels(C);
   const int P = NT * kGramK / C;
   const int64_t nchunks = (n_pix + P - 1) / P;
-  int64_t nb = 2 * (int64_t)num_sms();
+  int64_t nb = 4 * (int64_t)num_sms();
   if (nb > nchunks) nb = nchunks;
   if (nb < 1) nb = 1;
   return (int)nb;
@@ -296,6 +383,24 @@ static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *
 template <typename TIn, typename TO>
 static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const PcaParams &p,
                           void *out, void *stats, uint32_t *err, cudaStream_t st) {
+  if (p.C <= 16 && p.K <= 16) {
+    constexpr int PPT = 2;
+    const int NT = 256;
+    int64_t nb = (n_pix + (int64_t)NT * PPT - 1) / ((int64_t)NT * PPT);
+    const int64_t cap = 8 * (int64_t)num_sms() / (n_cubes > 0 ? n_cubes : 1) + 1;
+    if (nb > cap) nb = cap;
+    if (nb < 1) nb = 1;
+    dim3 grid((unsigned)nb, (unsigned)n_cubes);
+#define CV_PX(KB, CM) \
+  k_pca_project_px<TIn, TO, KB, CM, PPT><<<grid, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err)
+    if (p.C <= 8) {
+      if (p.K <= 8) CV_PX(8, 8); else CV_PX(16, 8);
+    } else {
+      if (p.K <= 8) CV_PX(8, 16); else CV_PX(16, 16);
+    }
+#undef CV_PX
+    return check_launch("cv_pca_project(px)");
+  }
   const int NT = threads_for_channels(p.C);
   const int P = NT * kGramK / p.C;
   const size_t sm = (size_t)P * (p.C + 1) * sizeof(double);
