@@ -74,13 +74,21 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
       if (a.ssim6) {
         const int ncg6 = (a.C + k6Chans - 1) / k6Chans;
         dim3 g6((unsigned)(ssim6_groups(a.W) * ncg6), (unsigned)a.T, (unsigned)n);
-        const size_t sm = sizeof(Ssim6Shared);
-        if (a.bit_depth <= 10) {
-          cudaFuncSetAttribute(k_eval_ssim6<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          k_eval_ssim6<RS, true><<<g6, 32 * 4 * k6Chans, sm, st>>>(a);
+        if (pca) {
+          if constexpr (RS == RS_FRAMES_U16) {
+            const size_t sm = sizeof(Ssim6SharedT<true>);
+            cudaFuncSetAttribute(k_eval_ssim6<RS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_eval_ssim6<RS, false, true><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
+          }
         } else {
-          cudaFuncSetAttribute(k_eval_ssim6<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          k_eval_ssim6<RS, false><<<g6, 32 * 4 * k6Chans, sm, st>>>(a);
+          const size_t sm = sizeof(Ssim6Shared);
+          if (a.bit_depth <= 10) {
+            cudaFuncSetAttribute(k_eval_ssim6<RS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_eval_ssim6<RS, true, false><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
+          } else {
+            cudaFuncSetAttribute(k_eval_ssim6<RS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_eval_ssim6<RS, false, false><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
+          }
         }
         return check_launch("cv_eval(ssim6)");
       }
@@ -218,7 +226,8 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, 
   a.TX = eval_tx(C, ssim);
   a.nstrips = (int)((W + a.TX - 1) / a.TX);
   // vertical-first SSIM kernel: frames, float32 original, no PCA, 4-byte aligned frame rows
-  a.ssim6 = ssim && frames && !pca && odtype == CV_F32 && W % 4 == 0 && !getenv("CVB_SSIM_V5");
+  a.ssim6 = ssim && frames && odtype == CV_F32 && W % 4 == 0 && !getenv("CVB_SSIM_V5") &&
+            (!pca || (fdtype == CV_U16 && E <= k6PcaMax));
   if (a.ssim6) a.nstrips = 4 * ssim6_groups(W);
   cudaStream_t st = (cudaStream_t)stream;
   int s;

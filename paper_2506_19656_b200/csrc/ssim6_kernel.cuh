@@ -45,7 +45,12 @@ constexpr int k6Stages = 8;     // input ring (rows), power of two
 constexpr int k6Depth = 6;      // input rows in flight per warp (< k6Stages)
 constexpr int k6Ring = 8;       // mbarrier-pipelined row ring
 
-struct Ssim6Shared {
+// PCA: the frames hold E <= k6PcaMax principal-component planes (12/16-bit);
+// every band's recon is mean_c + sum_j pc_j W[j][c] (transform.py:202-210).
+constexpr int k6PcaMax = 12;
+
+template <bool PCA>
+struct Ssim6SharedT {
   // column-filtered rows: [band][row slot e % 8][column % 4][column / 4]; a
   // sub-array pitch of 34 (= 2 mod 8) float4 makes both the producer stores
   // (lane = column) and the consumer loads (lane q reads column 4q+k) hit 32
@@ -54,9 +59,17 @@ struct Ssim6Shared {
   unsigned long long full[k6Chans][k6Ring];   // 4 warp arrivals: row stored
   unsigned long long empty[k6Chans][k6Ring];  // 1 arrival: row filtered
   float raw_o[2 * 4][k6Stages][32];
-  uint32_t raw_f[2 * 4][k6Stages][16];  // u16: 16 words; u8: <= 9 (rows may start 2 samples into a word)
-  double lut[k6Chans][k6LutMax];
+  // frame words of the warp's 32 columns: u16 -> 16 words per plane; u8 -> <= 9
+  // (rows may start 2 samples into a word); PCA: E planes of 16 words
+  uint32_t raw_f[2 * 4][k6Stages][PCA ? 16 * k6PcaMax : 16];
+  double lut[k6Chans][PCA ? 1 : k6LutMax];
+  // PCA: recon_c = base_c + sum_j q_j coef[c][j] with coef = (span_j / L) W[j][c]
+  // and base_c = mean_c + sum_j min_j W[j][c] (the dequantisation folded into
+  // the inverse projection; float64 throughout)
+  double coef[PCA ? k6Chans : 1][PCA ? k6PcaMax : 1];
+  double base[k6Chans];
 };
+using Ssim6Shared = Ssim6SharedT<false>;
 
 // Transposed-form 11-tap FIR along the rows of one column: z[k] holds the
 // partial sum of the output row completed k rows from now. One step consumes
@@ -104,13 +117,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity
 
 __host__ __device__ inline int ssim6_groups(int64_t W) { return (int)((W - 2 * kSsimRadius + k6Out - 1) / k6Out); }
 
-template <int RS, bool LUT>
+template <int RS, bool LUT, bool PCA>
 __global__ void __launch_bounds__(256, CVB_SSIM6_MINB)
-k_eval_ssim6(const EvalArgs args) {
+k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   using R = typename RawT<RS>::type;
   constexpr int FPW = (RS == RS_FRAMES_U8) ? 4 : 2;  // frame samples per 32-bit word
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Ssim6Shared &sh = *reinterpret_cast<Ssim6Shared *>(smem_raw);
+  Ssim6SharedT<PCA> &sh = *reinterpret_cast<Ssim6SharedT<PCA> *>(smem_raw);
+  static_assert(!PCA || (RS == RS_FRAMES_U16 && !LUT), "PCA path: u16 component planes");
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int j = w & 3, cl = w >> 2;
@@ -126,8 +140,23 @@ k_eval_ssim6(const EvalArgs args) {
   const bool last_grp = grp == (int)gridDim.x / ncg - 1;
   const double L = args.L, rL = args.rL;
 
+  const int E = args.E;
+  if constexpr (PCA) {
+    const int cc = cgrp * k6Chans + (int)threadIdx.x / k6PcaMax, jj = (int)threadIdx.x % k6PcaMax;
+    if (threadIdx.x < k6Chans * k6PcaMax && cc < C && jj < E) {
+      const double m = args.qmins[a * E + jj];
+      const double sp = __dsub_rn(args.qmaxs[a * E + jj], m);
+      sh.coef[threadIdx.x / k6PcaMax][jj] = (sp / L) * inv.W[jj * kMaxC + cc];
+    }
+    if (threadIdx.x < k6Chans && cgrp * k6Chans + (int)threadIdx.x < C) {
+      const int cb = cgrp * k6Chans + threadIdx.x;
+      double b = inv.mean[cb];
+      for (int j2 = 0; j2 < E; ++j2) b = __fma_rn(args.qmins[a * E + j2], inv.W[j2 * kMaxC + cb], b);
+      sh.base[threadIdx.x] = b;
+    }
+  }
   double my_m = 0.0, my_span = 0.0;
-  if (c < C) {
+  if (!PCA && c < C) {
     my_m = args.qmins[a * C + c];
     my_span = __dsub_rn(args.qmaxs[a * C + c], my_m);
   }
@@ -169,25 +198,46 @@ k_eval_ssim6(const EvalArgs args) {
   const int xc = vimg ? xv : W32 - 1;  // clamped column: loads stay in bounds
 
   const float *obase = reinterpret_cast<const float *>(args.orig) + (a * T + t) * inner + c;
-  const R *fbase = reinterpret_cast<const R *>(args.frames) + (((a * args.G + c / 3) * T + t) * 3 + c % 3) * HW;
+  // non-PCA: the band's own plane; PCA: plane (lane >> 4) (lane pairs of planes below)
+  const int fpl = PCA ? (lane >> 4) : c;
+  const R *fbase = reinterpret_cast<const R *>(args.frames) + (((a * args.G + fpl / 3) * T + t) * 3 + fpl % 3) * HW;
   // frame words: the warp's 32 samples start `foff` samples into the 4-byte word at xa
   const int xw = (int)x0 + 32 * j;
   const int xa = xw & ~(FPW - 1);
   const int foff = xw - xa;
-  const int fx = xa + lane * FPW;
-  const bool fok = lane < (foff + 32 + FPW - 1) / FPW && fx < W32;  // W % 4 == 0: words never straddle
+  const int fx = xa + (PCA ? (lane & 15) : lane) * FPW;
+  const bool fok = (PCA ? true : lane < (foff + 32 + FPW - 1) / FPW) && fx < W32;  // W % 4: words never straddle
+  // PCA: copy k of a row moves plane 2k + (lane >> 4), word lane & 15; the
+  // plane offset relative to plane lane >> 4 (planes j: video j/3, slot j%3)
+  auto pdelta = [&](int k) -> int64_t {
+    const int jj = 2 * k + (lane >> 4), j0 = lane >> 4;
+    return ((int64_t)(jj / 3 - j0 / 3) * 3 * T + (jj % 3 - j0 % 3)) * HW;
+  };
+  const int ncopy = (E + 1) / 2;  // PCA copies per lane and row
   const char *ip_o = reinterpret_cast<const char *>(obase + (int64_t)xc * C);
   const char *ip_f = reinterpret_cast<const char *>(fbase + (fok ? fx : 0));
   const int64_t ostride = rowlen * (int64_t)sizeof(float), fstride = W * (int64_t)sizeof(R);
   const uint32_t sa_o = smem_u32(&sh.raw_o[w][0][lane]);
-  const uint32_t sa_f = smem_u32(&sh.raw_f[w][0][lane]);
-  constexpr uint32_t kPO = 32 * sizeof(float), kPF = 16 * sizeof(uint32_t);
+  const uint32_t sa_f = smem_u32(&sh.raw_f[w][0][PCA ? 16 * (lane >> 4) + (lane & 15) : lane]);
+  constexpr uint32_t kPO = 32 * sizeof(float), kPF = (PCA ? 16 * k6PcaMax : 16) * sizeof(uint32_t);
+  auto copy_frames = [&](uint32_t soff) {
+    if constexpr (PCA) {
+#pragma unroll
+      for (int k = 0; k < (k6PcaMax + 1) / 2; ++k)
+        if (k < ncopy && (2 * k + (lane >> 4) < E) && fok)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + soff + k * 32 * 4),
+                       "l"(ip_f + pdelta(k) * (int64_t)sizeof(R))
+                       : "memory");
+    } else {
+      if (fok) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + soff), "l"(ip_f) : "memory");
+    }
+  };
   const int H32 = (int)H;
   // copy row yi into stage yi % k6Stages (rows past the frame: empty group)
   auto issue_s = [&](auto scst) {  // steady state: the row exists, stage S static
     constexpr uint32_t S = decltype(scst)::value;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_o + S * kPO), "l"(ip_o) : "memory");
-    if (fok) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + S * kPF), "l"(ip_f) : "memory");
+    copy_frames(S * kPF);
     ip_o += ostride;
     ip_f += fstride;
     cp_async_commit();
@@ -196,8 +246,7 @@ k_eval_ssim6(const EvalArgs args) {
     if (yi < H32) {
       const uint32_t s = (uint32_t)yi & (k6Stages - 1);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_o + s * kPO), "l"(ip_o) : "memory");
-      if (fok)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + s * kPF), "l"(ip_f) : "memory");
+      copy_frames(s * kPF);
     }
     ip_o += ostride;
     ip_f += fstride;
@@ -216,10 +265,28 @@ k_eval_ssim6(const EvalArgs args) {
   // convert row y (stage y % k6Stages) into (s, d); SSE + recon write
   auto convert = [&](int st, float &sv, float &dv) {
     const float om = sh.raw_o[w][st][lane];
-    const uint32_t q = (sh.raw_f[w][st][fw] >> fsh) & ((1u << (32 / FPW)) - 1u);
     double rm;
-    if constexpr (LUT) rm = sh.lut[cl][min(q, (uint32_t)(k6LutMax - 1))];
-    else rm = dequantize_fast(q, my_m, my_span, L, rL);
+    uint32_t q;
+    if constexpr (PCA) {
+      // recon = mean_c + sum_j pc_j W[j][c] with pc_j = min_j + q_j span_j / L,
+      // reassociated (base + sum q_j coef_j): agrees with the reference's
+      // float64 evaluation to ~1e-16 relative
+      double acc = sh.base[cl];
+      q = 0;
+#pragma unroll
+      for (int jj = 0; jj < k6PcaMax; ++jj) {
+        if (jj < E) {
+          const uint32_t qj = (sh.raw_f[w][st][16 * jj + fw] >> fsh) & 0xffffu;
+          q = max(q, qj);
+          acc = __fma_rn((double)qj, sh.coef[cl][jj], acc);
+        }
+      }
+      rm = acc;
+    } else {
+      q = (sh.raw_f[w][st][fw] >> fsh) & ((1u << (32 / FPW)) - 1u);
+      if constexpr (LUT) rm = sh.lut[cl][min(q, (uint32_t)(k6LutMax - 1))];
+      else rm = dequantize_fast(q, my_m, my_span, L, rL);
+    }
     const double diff = __dsub_rn((double)om, rm);
     const float df = (float)diff;
     qmax = max(qmax, vimg ? q : 0u);

@@ -258,7 +258,10 @@ def test_stream_zero_pad_and_noisy_frames(cuda, golden):
 
 @pytest.mark.parametrize("shape,C_pcs,B", [((6, 13, 17, 1), 0, 8), ((4, 12, 12, 32), 0, 12),
                                            ((3, 15, 19, 5), 0, 16), ((2, 21, 11, 12), 9, 12),
-                                           ((5, 11, 30, 4), 2, 16)])
+                                           ((5, 11, 30, 4), 2, 16),
+                                           # W % 4 == 0: PCA inverse inside the vertical-first SSIM kernel
+                                           ((2, 20, 132, 12), 9, 12), ((1, 16, 248, 5), 4, 16),
+                                           ((1, 13, 128, 12), 12, 16)])
 def test_stream_edge_shapes(cuda, shape, C_pcs, B):
     rng = np.random.default_rng(11)
     x = (rng.random(shape) * 3 - 1).astype(np.float32)
