@@ -12,19 +12,20 @@
 
 namespace cvb {
 
-constexpr int kGramK = 4;  // elements per thread per chunk
+constexpr int kGramK = 4;   // elements per thread per chunk (projection)
+constexpr int kGramKG = 16; // elements per thread per chunk (Gram): 4x the work per barrier
 
 // Gram partial of one CTA over a grid-stride set of pixel chunks.
 // Staging: thread-owns-elements (band tid % C) -> shifted f64 in smem;
 // accumulation: 4x4 tiles of the upper block triangle, one tile per thread,
 // pixels strided over the lanes sharing a tile.
-template <typename TIn>
-__global__ void __launch_bounds__(1024)
+template <typename TIn, int MAXT>
+__global__ void __launch_bounds__(MAXT)
 k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ partials,
        StatsEntry *__restrict__ stats, uint32_t *err) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int NT = blockDim.x, tid = threadIdx.x;
-  const int P = NT * kGramK / C;
+  const int P = NT * kGramKG / C;
   const int CS = C + 1;  // padded row stride
   double *xs = reinterpret_cast<double *>(smem);  // [P][CS]
   const int nb = (C + 3) / 4;
@@ -59,10 +60,10 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
   const int64_t ne = n_pix * C;
   // register prefetch of the next chunk (the staging barrier no longer
   // exposes the full load latency per chunk)
-  TIn nxt[kGramK];
+  TIn nxt[kGramKG];
   auto fetch = [&](int64_t ch) {
 #pragma unroll
-    for (int k = 0; k < kGramK; ++k) {
+    for (int k = 0; k < kGramKG; ++k) {
       const int64_t e = ch * P * C + tid + k * NT;
       nxt[k] = (ch < nchunks && e < ne) ? ldg(src + e) : TIn(0);
     }
@@ -71,13 +72,13 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t pix0 = ch * P;
     const int64_t e0 = pix0 * C;
-    TIn cur[kGramK];
+    TIn cur[kGramKG];
 #pragma unroll
-    for (int k = 0; k < kGramK; ++k) cur[k] = nxt[k];
+    for (int k = 0; k < kGramKG; ++k) cur[k] = nxt[k];
     fetch(ch + gridDim.x);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kGramK; ++k) {
+    for (int k = 0; k < kGramKG; ++k) {
       const int el = tid + k * NT;
       const int64_t e = e0 + el;
       double d = 0.0;
@@ -351,7 +352,7 @@ static int num_sms() {
 
 static int gram_blocks(int64_t n_pix, int C) {
   const int NT = threads_for_channels(C);
-  const int P = NT * kGramK / C;
+  const int P = NT * kGramKG / C;
   const int64_t nchunks = (n_pix + P - 1) / P;
   int64_t nb = 4 * (int64_t)num_sms();
   if (nb > nchunks) nb = nchunks;
@@ -363,14 +364,14 @@ template <typename TIn>
 static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *out, void *stats,
                        uint32_t *err, cudaStream_t st) {
   const int NT = threads_for_channels(C);
-  const int P = NT * kGramK / C;
+  const int P = NT * kGramKG / C;
   const int nb = (C + 3) / 4, ntile = nb * (nb + 1) / 2;
   size_t sm = (size_t)P * (C + 1) * sizeof(double);
   size_t sm2 = (size_t)NT * 16 * sizeof(double);  // tile reduction (>= ntile*nlanes*16)
   (void)ntile;
   if (sm2 > sm) sm = sm2;
   const int nblk = gram_blocks(n_pix, C);
-  auto kern = k_gram<TIn>;
+  auto kern = NT <= 512 ? k_gram<TIn, 512> : k_gram<TIn, 1024>;
   if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   kern<<<nblk, NT, sm, st>>>((const TIn *)src, n_pix, C, (double *)ws, (StatsEntry *)stats, err);
   int s = check_launch("cv_pca_gram");
