@@ -330,10 +330,6 @@ def run_ours(a):
     stream = torch.cuda.current_stream(dev)
     wsp = pipeline.Workspace()
 
-    # dense filled cube: the sparse patch (encode_prep(sparse_fill=True)) saves ~3 B/elem of
-    # HBM writes but puts a dependent load on the decode's critical path for every missing
-    # value (20 % of the frames here): measured slower (46.98 vs 34.46 ms per step)
-    sparse = False
     phases = ("stats", "quantize", "eval")
     ev = []
 
@@ -350,7 +346,7 @@ def run_ours(a):
                 e.record(stream)
                 marks[label] = e
 
-        enc = pipeline.encode_prep(x, spec, marks=mark, shard=shard, workspace=wsp, sparse_fill=sparse)
+        enc = pipeline.encode_prep(x, spec, marks=mark, shard=shard, workspace=wsp)
         mark("quantize")
         _, sc = pipeline.decode_eval(enc, x, recon_out=recon, want_ssim=wl.ssim)
         mark("eval")

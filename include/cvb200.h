@@ -143,9 +143,6 @@ int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner,
  * carry_in (nullable [n_cubes][HW*C]: carries from earlier time shards);
  * filled_out (nullable, f32 input only) then receives the filled cube, i.e.
  * forward_fill_time's output (cube.py:244-246), in the same pass.
- * fill_mode 2 fills the same way but may write filled_out only where the
- * source is NaN (a sparse patch for cv_eval_patched; skips ~4 bytes of HBM
- * writes per element when observations dominate).
  * out_layout CHANNEL_LAST: out [n_cubes][T][HW][E] (what quantize returns).
  * out_layout PLANAR: out [n_cubes][G][T][3][HW], planes padded per pad_mode
  *   (plan.py:118-128 + bridge.py:157-160).
@@ -244,21 +241,6 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins,
             int64_t H, int64_t W, int32_t C, const double *peaks,
             int32_t want_ssim, float *recon_out, void *ws, double *sse,
             double *ssim_sum, uint32_t *err_word, void *stream);
-
-/*
- * cv_eval with the original given as the raw cube (NaN = missing) plus the
- * sparse fill patch cv_quantize(fill_mode 2) wrote: wherever orig is NaN the
- * scored value is fill_patch at the same index (same layout as orig). Only
- * for a float32 original without PCA (SSIM additionally needs W % 4 == 0);
- * otherwise CV_ERR_UNSUPPORTED. fill_patch NULL == cv_eval.
- */
-int cv_eval_patched(const void *frames, int32_t fdtype, int32_t E, const double *qmins,
-                    const double *qmaxs, int32_t bit_depth, const double *inv_mean,
-                    const double *inv_comps, const void *recon_in, int32_t rdtype,
-                    const void *orig, int32_t odtype, const float *fill_patch,
-                    int64_t n_cubes, int64_t T, int64_t H, int64_t W, int32_t C,
-                    const double *peaks, int32_t want_ssim, float *recon_out, void *ws,
-                    double *sse, double *ssim_sum, uint32_t *err_word, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* spectral angle                           */

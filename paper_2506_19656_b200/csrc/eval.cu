@@ -163,11 +163,10 @@ size_t cv_eval_ws_bytes(int64_t n_cubes, int64_t T, int64_t H, int64_t W, int32_
   return (size_t)(n_cubes * T * nstrips * 2 * C) * sizeof(double);
 }
 
-int cv_eval_patched(const void *frames, int32_t fdtype, int32_t E, const double *qmins, const double *qmaxs,
-                    int32_t bit_depth, const double *inv_mean, const double *inv_comps, const void *recon_in,
-                    int32_t rdtype, const void *orig, int32_t odtype, const float *fill_patch, int64_t n_cubes,
-                    int64_t T, int64_t H, int64_t W, int32_t C, const double *peaks, int32_t want_ssim,
-                    float *recon_out, void *ws,
+int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, const double *qmaxs,
+            int32_t bit_depth, const double *inv_mean, const double *inv_comps, const void *recon_in,
+            int32_t rdtype, const void *orig, int32_t odtype, int64_t n_cubes, int64_t T, int64_t H,
+            int64_t W, int32_t C, const double *peaks, int32_t want_ssim, float *recon_out, void *ws,
             double *sse, double *ssim_sum, uint32_t *err_word, void *stream) {
   if (!orig || !ws) return fail(CV_ERR_ARG, "cv_eval: null pointer");
   if ((frames == nullptr) == (recon_in == nullptr))
@@ -230,12 +229,6 @@ int cv_eval_patched(const void *frames, int32_t fdtype, int32_t E, const double 
   a.ssim6 = ssim && frames && odtype == CV_F32 && W % 4 == 0 && !getenv("CVB_SSIM_V5") &&
             (!pca || (fdtype == CV_U16 && E <= k6PcaMax));
   if (a.ssim6) a.nstrips = 4 * ssim6_groups(W);
-  a.patch = fill_patch;
-  // the sparse-fill read is implemented by the float32 vertical-first SSIM
-  // kernel and the PSNR-only kernel (without PCA)
-  if (fill_patch && (odtype != CV_F32 || pca || (ssim && !a.ssim6)))
-    return fail(CV_ERR_UNSUPPORTED, "cv_eval_patched: sparse fill needs a float32 original, no PCA and "
-                "(for SSIM) W %% 4 == 0");
   cudaStream_t st = (cudaStream_t)stream;
   int s;
   switch (odtype) {
@@ -250,17 +243,6 @@ int cv_eval_patched(const void *frames, int32_t fdtype, int32_t E, const double 
   k_eval_finalize<<<(unsigned)((nwarps * 32 + 255) / 256), 256, 0, st>>>((const double *)ws, n_cubes,
                                                                          nper, C, sse, ssim_sum);
   return check_launch("cv_eval(finalize)");
-}
-
-
-int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, const double *qmaxs,
-            int32_t bit_depth, const double *inv_mean, const double *inv_comps, const void *recon_in,
-            int32_t rdtype, const void *orig, int32_t odtype, int64_t n_cubes, int64_t T, int64_t H,
-            int64_t W, int32_t C, const double *peaks, int32_t want_ssim, float *recon_out, void *ws,
-            double *sse, double *ssim_sum, uint32_t *err_word, void *stream) {
-  return cv_eval_patched(frames, fdtype, E, qmins, qmaxs, bit_depth, inv_mean, inv_comps, recon_in, rdtype,
-                         orig, odtype, nullptr, n_cubes, T, H, W, C, peaks, want_ssim, recon_out, ws, sse,
-                         ssim_sum, err_word, stream);
 }
 
 }  // extern "C"

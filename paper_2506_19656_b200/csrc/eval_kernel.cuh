@@ -36,7 +36,6 @@ struct EvalArgs {
   uint32_t *err;
   int TX, nstrips;
   int ssim6;  // launch k_eval_ssim6 (nstrips = 4 * ssim6_groups(W))
-  const float *patch;  // sparse fill values (same layout as orig, read where orig is NaN) or null
 };
 
 enum { RS_FRAMES_U8 = 0, RS_FRAMES_U16 = 1, RS_RECON_F32 = 2, RS_RECON_F64 = 3 };
@@ -203,11 +202,6 @@ k_eval(const EvalArgs args, const PcaParams inv) {
   R r_m = R(0), r_h = R(0), r_mn = R(0), r_hn = R(0);
   auto load_next = [&]() {
     o_mn = ldg(op_m);
-    if constexpr (std::is_same<TO, float>::value && !SSIM) {
-      // sparse fill: the forward-filled value of a missing observation
-      if (args.patch != nullptr && o_mn != o_mn)
-        o_mn = ldg(args.patch + (op_m - reinterpret_cast<const float *>(args.orig)));
-    }
     op_m += rowlen;
     if constexpr (!PCA) {
       r_mn = ldg(rp_m);

@@ -50,7 +50,6 @@ struct QuantArgs {
   const float *seg_last;
   const float *carry_in;  // [n_cubes][inner] carries from earlier time shards (nullable)
   float *filled_out;
-  int fill_sparse;  // fill_mode 2: filled_out written only where the source is NaN
   uint32_t *err;
 };
 
@@ -542,7 +541,6 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int6
     return fail(CV_ERR_UNSUPPORTED, "cv_quantize: grid too large");
   const bool pca = pca_comps != nullptr;
   const bool fill = fill_mode != 0;
-  if (fill_mode < 0 || fill_mode > 2) return fail(CV_ERR_ARG, "cv_quantize: fill_mode %d not in 0..2", fill_mode);
   if (fill && (dtype != CV_F32 || !seg_last))
     return fail(CV_ERR_ARG, "cv_quantize: fill_mode needs f32 input and a seg_last map");
   if (out_layout != CV_LAYOUT_CHANNEL_LAST && out_layout != CV_LAYOUT_PLANAR)
@@ -572,7 +570,6 @@ int cv_quantize(const void *src, int32_t dtype, int64_t n_cubes, int64_t T, int6
   a.seg_last = seg_last;
   a.carry_in = fill ? carry_in : nullptr;
   a.filled_out = fill ? filled_out : nullptr;
-  a.fill_sparse = fill_mode == 2;
   a.err = err_word;
   cudaStream_t st = (cudaStream_t)stream;
   const bool planar = out_layout == CV_LAYOUT_PLANAR;

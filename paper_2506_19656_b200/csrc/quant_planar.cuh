@@ -120,25 +120,14 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
           const int v = tid + i * NT;
           float4 x = *reinterpret_cast<float4 *>(st + v * 4);
           float xv[4] = {x.x, x.y, x.z, x.w};
-          bool miss[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            miss[j] = isnan(xv[j]);
-            if (miss[j]) xv[j] = carry[i * 4 + j];
+            if (isnan(xv[j])) xv[j] = carry[i * 4 + j];
             else carry[i * 4 + j] = xv[j];
           }
           x = make_float4(xv[0], xv[1], xv[2], xv[3]);
           *reinterpret_cast<float4 *>(st + v * 4) = x;
-          if (fo) {
-            if (!args.fill_sparse) {
-              *reinterpret_cast<float4 *>(fo + v * 4) = x;
-            } else if (miss[0] | miss[1] | miss[2] | miss[3]) {
-              // sparse fill: only the filled-in values (decode reads them where the source is NaN)
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (miss[j]) fo[v * 4 + j] = xv[j];
-            }
-          }
+          if (fo) *reinterpret_cast<float4 *>(fo + v * 4) = x;
         }
       }
     }

@@ -263,10 +263,8 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   float ssum = 0.f;
 
   // convert row y (stage y % k6Stages) into (s, d); SSE + recon write
-  const int64_t pbase = (a * T + t) * inner + (int64_t)xc * C + c;  // sparse-fill element offset
-  auto convert = [&](int st, int yr, float &sv, float &dv) {
-    float om = sh.raw_o[w][st][lane];
-    if (args.patch != nullptr && om != om) om = __ldg(args.patch + pbase + (int64_t)yr * rowlen);
+  auto convert = [&](int st, float &sv, float &dv) {
+    const float om = sh.raw_o[w][st][lane];
     double rm;
     uint32_t q;
     if constexpr (PCA) {
@@ -310,7 +308,7 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   float sv_n, dv_n;
   cp_async_wait<k6Depth - 1>();
   __syncwarp();
-  convert(0, 0, sv_n, dv_n);  // stage 0
+  convert(0, sv_n, dv_n);  // stage 0
 
   // mbarrier pipeline: every warp stores column-filtered row e into ring slot
   // e % 8 (after the slot's previous row was filtered: empty barrier) and
@@ -359,7 +357,7 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
     if (y + 1 < H32) {
       cp_async_wait<k6Depth - 1>();
       __syncwarp();
-      convert((y + 1) & (k6Stages - 1), y + 1, sv_n, dv_n);
+      convert((y + 1) & (k6Stages - 1), sv_n, dv_n);
     }
     const float4 o = fir4_step(fir, sv, dv);
     if (y >= 2 * kSsimRadius) {
@@ -381,7 +379,7 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
     issue_s(std::integral_constant<uint32_t, (P + k6Depth) % k6Stages>{});
     cp_async_wait<k6Depth - 1>();
     __syncwarp();
-    convert((P + 1) % k6Stages, y + 1, sv_n, dv_n);
+    convert((P + 1) % k6Stages, sv_n, dv_n);
     const float4 o = fir4_step(fir, sv, dv);
     const int e = y - 2 * kSsimRadius;
     mbar_wait(&sh.empty[cl][SL], (uint32_t)(e >> 3) & 1u);

@@ -83,7 +83,6 @@ class Encoded:
     pca: list = field(default_factory=list)   # one PcaFold per cube
     err: dev.ErrWord | None = None
     filled: torch.Tensor | None = None   # forward-filled cube (float32 sources)
-    fill_patch: torch.Tensor | None = None  # sparse fill: filled values where the source is NaN
     t_total: int | None = None           # frames over all time shards (multi-GPU)
     shard: object | None = None          # dist.TimeShard of a time-sharded stream
 
@@ -198,17 +197,13 @@ def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normaliz
 
 
 def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | None = None,
-                shard=None, workspace: Workspace | None = None, sparse_fill: bool = False) -> Encoded:
+                shard=None, workspace: Workspace | None = None) -> Encoded:
     """Cube(s) -> planar integer frames + QuantParams (+ PCA models).
 
     Float32 cubes are forward-filled on the fly; the quantiser also writes the
     filled cube (``Encoded.filled``, forward_fill_time's output) so decode can
-    score against what the codec saw. With ``sparse_fill`` it writes only the
-    filled-in values (``Encoded.fill_patch``, valid where the source is NaN)
-    and decode scores against the source plus that patch (pass the source to
-    ``decode_eval``) -- the same scores for ~4 fewer HBM bytes per element.
-    ``marks`` (optional callable) is invoked with a phase label after the
-    statistics phase (benchmark CUDA events).
+    score against what the codec saw. ``marks`` (optional callable) is invoked
+    with a phase label after the statistics phase (benchmark CUDA events).
     """
     x, (B, T, H, W, C) = _as_batch(cube)
     d = x.device
@@ -276,8 +271,7 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
     for b in range(B) if spec.n_pcs else [None]:
         if b is None:
             _lib.call("cv_quantize", x.ptr, x.code, B, T, HW, C, qmins.data_ptr(), qmaxs.data_ptr(),
-                      spec.bit_depth, int(spec.clamp), (2 if sparse_fill else 1) if fill else 0,
-                      float(spec.fill_value), seg,
+                      spec.bit_depth, int(spec.clamp), int(fill), float(spec.fill_value), seg,
                       seg_last.data_ptr() if seg_last is not None else None,
                       carry_in.data_ptr() if carry_in is not None else None, None, None, 0,
                       _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames.data_ptr(),
@@ -290,11 +284,8 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
                       fold.fwd_mean.ctypes.data, fold.fwd_comps.ctypes.data, E,
                       _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames[b].data_ptr(), None,
                       err.ptr, s)
-    patch = None
-    if sparse_fill and filled is not None:
-        filled, patch = None, filled
     enc = Encoded(frames, qmins, qmaxs, spec, (B, T, H, W, C), groups, peaks, nans, seg_last,
-                  folds, err, filled, patch)
+                  folds, err, filled)
     if sharded:
         tt = torch.tensor([T], dtype=torch.int64, device=d)
         shard.all_reduce(tt)
@@ -342,12 +333,9 @@ def decode_eval(enc: Encoded, orig=None, frames: torch.Tensor | None = None, wan
     ``enc.filled`` when the encoder produced it, else ``orig``.
     """
     B, T, H, W, C = enc.shape
-    patch = enc.fill_patch
     ref = enc.filled if enc.filled is not None else orig
     if ref is None:
         raise ConfigurationError("decode_eval needs the original cube to score against")
-    if patch is not None and enc.filled is None and orig is None:
-        raise ConfigurationError("decode_eval with a sparse fill patch needs the source cube")
     o, shp = _as_batch(ref)
     if shp != enc.shape:
         raise ConfigurationError(f"original {shp} does not match the encoded stream {enc.shape}")
@@ -370,9 +358,8 @@ def decode_eval(enc: Encoded, orig=None, frames: torch.Tensor | None = None, wan
     err = enc.err if enc.err is not None else dev.ErrWord(d)
     fdt = _lib.CV_U8 if fr.dtype == torch.uint8 else _lib.CV_U16
     if not enc.pca:
-        _lib.call("cv_eval_patched", fr.data_ptr(), fdt, E, enc.qmins.data_ptr(), enc.qmaxs.data_ptr(),
-                  enc.spec.bit_depth, None, None, None, 0, o.ptr, o.code,
-                  patch.data_ptr() if patch is not None else None, B, T, H, W, C,
+        _lib.call("cv_eval", fr.data_ptr(), fdt, E, enc.qmins.data_ptr(), enc.qmaxs.data_ptr(),
+                  enc.spec.bit_depth, None, None, None, 0, o.ptr, o.code, B, T, H, W, C,
                   enc.peaks.data_ptr(), int(want_ssim), recon.data_ptr() if recon is not None else None,
                   ws.data_ptr(), sse.data_ptr(), ssum.data_ptr(), err.ptr, s)
     else:
@@ -397,20 +384,11 @@ def decode_eval(enc: Encoded, orig=None, frames: torch.Tensor | None = None, wan
     return recon, scores
 
 
-def sparse_fill_ok(shape, spec: StreamSpec, want_ssim: bool) -> bool:
-    """Whether decode_eval can score a sparse fill patch for this stream
-    (cv_eval_patched: no PCA; SSIM needs W % 4 == 0)."""
-    W = shape[-2]
-    return spec.n_pcs == 0 and (not want_ssim or W % 4 == 0)
-
-
-def roundtrip(cube, spec: StreamSpec, want_ssim: bool = True, want_recon: bool = True,
-              sparse_fill: bool = False):
+def roundtrip(cube, spec: StreamSpec, want_ssim: bool = True, want_recon: bool = True):
     """encode_prep -> (identity codec) -> decode_eval; returns (encoded, recon, scores)."""
     if not dev.is_device_tensor(cube):
         cube = dev.to_device(cube).t
-    sparse = sparse_fill and sparse_fill_ok(tuple(cube.shape), spec, want_ssim)
-    enc = encode_prep(cube, spec, sparse_fill=sparse)
+    enc = encode_prep(cube, spec)
     recon, scores = decode_eval(enc, cube, want_ssim=want_ssim, want_recon=want_recon)
     return enc, recon, scores
 
@@ -424,10 +402,9 @@ class HostStreamer:
     """
 
     def __init__(self, shape, dtype, spec: StreamSpec, chunk: int, want_ssim: bool = True,
-                 device=None, sparse_fill: bool = False):
+                 device=None):
         self.B, self.T, self.H, self.W, self.C = shape
         self.spec = spec
-        self.sparse_fill = sparse_fill and sparse_fill_ok(tuple(shape), spec, want_ssim)
         self.chunk = max(1, min(chunk, self.B))
         self.want_ssim = want_ssim
         self.device = device or dev.default_device()
@@ -469,7 +446,7 @@ class HostStreamer:
                 issue(i + 1)
             comp.wait_event(self.ready[k])
             x = self.bufs[k][:n]
-            enc = encode_prep(x, self.spec, workspace=self.ws[k], sparse_fill=self.sparse_fill)
+            enc = encode_prep(x, self.spec, workspace=self.ws[k])
             _, scores = decode_eval(enc, x, want_ssim=self.want_ssim, recon_out=self.recon[:n])
             self.free[k].record(comp)
             sse.append(scores.sse)

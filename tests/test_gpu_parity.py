@@ -346,31 +346,3 @@ def test_ssim_column_groups(cuda, shape, B):
     rep = sc.report()[0]
     np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), rtol=1e-9)
     np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
-
-
-@pytest.mark.parametrize("shape,B,ssim", [((30, 16, 20, 7), 10, True), ((24, 13, 12, 3), 8, False),
-                                          ((18, 12, 36, 5), 16, True), ((9, 11, 20, 2), 12, False)])
-def test_sparse_fill_patch(cuda, shape, B, ssim):
-    """fill_mode 2 + cv_eval_patched: decode scores the source plus the sparse
-    patch exactly like the dense filled cube (leading gaps, whole NaN frames,
-    scattered NaN pixels)."""
-    rng = np.random.default_rng(sum(shape) + B)
-    x = (rng.random(shape) * 2 + 0.5).astype(np.float32)
-    x[rng.random(shape[:1]) < 0.3] = np.nan
-    x[rng.random(shape) < 0.05] = np.nan
-    x[:2, :3, :4, 0] = np.nan
-    xd = torch.from_numpy(x).to(cuda)
-    spec = G_pipe.StreamSpec(B)
-    enc_d, rec_d, sc_d = G_pipe.roundtrip(xd, spec, want_ssim=ssim)
-    enc_s, rec_s, sc_s = G_pipe.roundtrip(xd, spec, want_ssim=ssim, sparse_fill=True)
-    assert enc_s.fill_patch is not None and enc_s.filled is None
-    np.testing.assert_array_equal(enc_s.frames.cpu().numpy(), enc_d.frames.cpu().numpy())
-    np.testing.assert_array_equal(rec_s.cpu().numpy(), rec_d.cpu().numpy())
-    rd, rs = sc_d.report()[0], sc_s.report()[0]
-    np.testing.assert_array_equal(rs["psnr_per_band"], rd["psnr_per_band"])
-    if ssim:
-        np.testing.assert_array_equal(rs["ssim_per_band"], rd["ssim_per_band"])
-    ref = O.encode_stream(x, B)
-    np.testing.assert_allclose(rs["psnr_per_band"],
-                               M.psnr_per_band(ref["filled"], O.decode_stream(ref["frames"], ref, x.shape, B)),
-                               rtol=1e-9)
