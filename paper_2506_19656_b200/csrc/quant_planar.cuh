@@ -33,6 +33,7 @@ __device__ __forceinline__ void cp_async_wait_q() {
 // 2p+1, keeps every band's float32 quantiser constants in registers and
 // stores both samples of a plane with one 32-bit (u16) / 16-bit (u8) store.
 constexpr int kQRegC = 8;
+constexpr int kQPcaC = 16;  // PCA register path: channels and components
 
 template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false>
 __global__ void __launch_bounds__(256)
@@ -195,6 +196,33 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
             o[jp * HW] = (TOut)q;
           }
           o += gstride;
+        }
+      } else if (C <= kQPcaC && E <= kQPcaC) {
+        // registers only: C differences, K components with constant-bank
+        // weights (static indices), incremental plane pointer
+        double d[kQPcaC];
+#pragma unroll
+        for (int c = 0; c < kQPcaC; ++c) d[c] = c < C ? __dsub_rn((double)px[c], pca.mean[c]) : 0.0;
+        uint32_t last = 0;
+        TOut *op = o;
+#pragma unroll
+        for (int pl = 0; pl < 3 * ((kQPcaC + 2) / 3); ++pl) {
+          if (pl < 3 * args.G) {
+            uint32_t q;
+            if (pl < E) {
+              double pc = 0.0;
+#pragma unroll
+              for (int c = 0; c < kQPcaC; ++c)
+                if (c < C) pc = __fma_rn(d[c], pca.W[pl * kMaxC + c], pc);
+              const QBand b = qtab[pl];
+              q = quantize_value(range_prep(pc, b, args.clamp, bad), b);
+              last = q;
+            } else {
+              q = args.pad_mode == CV_PAD_REPEAT ? last : 0u;
+            }
+            *op = (TOut)q;
+            op += (pl % 3 == 2) ? gjump : HW;
+          }
         }
       } else {
         double d[kMaxC];
