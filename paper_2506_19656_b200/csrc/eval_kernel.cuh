@@ -69,15 +69,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
 //   sigma_x^2+sigma_y^2 = (vs+vd)/2, 2 sigma_xy = (vs-vd)/2,
 // written as l = 1 - md^2/den_l, cs = 1 - vd/den_c so the float32 rounding
 // only touches the small difference terms. C1, C2 > 0 keep den_l, den_c > 0.
+// mu_x^2 + mu_y^2 = (u^2 + md^2)/2 with u = ms + 2 c0 (13 instructions).
 __device__ __forceinline__ float ssim_px(float ms, float md, float ess, float edd, float c0,
                                          float C1, float C2) {
-  const float mx = fmaf(0.5f, ms + md, c0);
-  const float my = fmaf(0.5f, ms - md, c0);
+  const float u = fmaf(2.f, c0, ms);
+  const float md2 = md * md;
   const float vd = fmaf(-md, md, edd);
   const float vs = fmaf(-ms, ms, ess);
-  const float den_l = fmaf(mx, mx, fmaf(my, my, C1));
+  const float den_l = fmaf(0.5f, fmaf(u, u, md2), C1);
   const float den_c = fmaf(0.5f, vs + vd, C2);
-  const float l = fmaf(-md * md, rcp_approx(den_l), 1.f);
+  const float l = fmaf(-md2, rcp_approx(den_l), 1.f);
   const float cs = fmaf(-vd, rcp_approx(den_c), 1.f);
   return l * cs;
 }

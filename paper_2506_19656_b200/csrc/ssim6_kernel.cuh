@@ -206,7 +206,10 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   const int xa = xw & ~(FPW - 1);
   const int foff = xw - xa;
   const int fx = xa + (PCA ? (lane & 15) : lane) * FPW;
-  const bool fok = (PCA ? true : lane < (foff + 32 + FPW - 1) / FPW) && fx < W32;  // W % 4: words never straddle
+  // words past the row end copy the row's last word instead (valid samples for
+  // lanes outside the frame, whose results are never counted)
+  const bool fok = PCA ? true : lane < (foff + 32 + FPW - 1) / FPW;
+  const int fxc = min(fx, W32 - FPW);  // W % 4 == 0: words never straddle the row end
   // PCA: copy k of a row moves plane 2k + (lane >> 4), word lane & 15; the
   // plane offset relative to plane lane >> 4 (planes j: video j/3, slot j%3)
   auto pdelta = [&](int k) -> int64_t {
@@ -215,7 +218,7 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   };
   const int ncopy = (E + 1) / 2;  // PCA copies per lane and row
   const char *ip_o = reinterpret_cast<const char *>(obase + (int64_t)xc * C);
-  const char *ip_f = reinterpret_cast<const char *>(fbase + (fok ? fx : 0));
+  const char *ip_f = reinterpret_cast<const char *>(fbase + (fok ? fxc : 0));
   const int64_t ostride = rowlen * (int64_t)sizeof(float), fstride = W * (int64_t)sizeof(R);
   const uint32_t sa_o = smem_u32(&sh.raw_o[w][0][lane]);
   const uint32_t sa_f = smem_u32(&sh.raw_f[w][0][PCA ? 16 * (lane >> 4) + (lane & 15) : lane]);
@@ -287,13 +290,15 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
       if constexpr (LUT) rm = sh.lut[cl][min(q, (uint32_t)(k6LutMax - 1))];
       else rm = dequantize_fast(q, my_m, my_span, L, rL);
     }
+    // lanes outside the frame (or owned by the next CTA) compute on valid
+    // neighbour samples: their maps only reach masked outputs and their SSE
+    // is dropped at the end
     const double diff = __dsub_rn((double)om, rm);
     const float df = (float)diff;
-    qmax = max(qmax, vimg ? q : 0u);
-    sv = vimg ? fmaf(2.f, om - c0, -df) : 0.f;
-    dv = vimg ? df : 0.f;
-    const double dm = own ? diff : 0.0;
-    sse = __fma_rn(dm, dm, sse);
+    qmax = max(qmax, q);
+    sv = fmaf(2.f, om - c0, -df);
+    dv = df;
+    sse = __fma_rn(diff, diff, sse);
     if (wr) *wq = (float)rm;
     wq += rowlen;
   };
@@ -416,6 +421,7 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
     if (j == (e & 3)) consume(e);
     ssum_d += (double)ssum;
   }
+  if (!own) sse = 0.0;
   flag_warp(args.err, qmax > args.Li, CV_FLAG_INT_RANGE);
 
 #pragma unroll
