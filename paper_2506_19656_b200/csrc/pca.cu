@@ -251,7 +251,7 @@ k_pca_project(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
 // with constant-bank weights; per-component min/max in registers. Several
 // pixels per thread are in flight (PPT) to cover the load latency.
 template <typename TIn, typename TO, int KB, int CM, int PPT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (CM <= 12 && KB <= 8) ? 2 : 1)
 k_pca_project_px(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
                  StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err) {
   const int C = pca.C, K = pca.K;
@@ -270,6 +270,20 @@ k_pca_project_px(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ ou
 #pragma unroll
     for (int u = 0; u < PPT; ++u) {
       const int64_t pix = p0 + (int64_t)u * blockDim.x;
+      if constexpr (std::is_same<TIn, float>::value && CM % 4 == 0) {
+        if (C == CM) {  // whole pixel as CM/4 16-byte loads (pixel rows are 16-byte aligned)
+#pragma unroll
+          for (int c4 = 0; c4 < CM / 4; ++c4) {
+            const float4 q = pix < n_pix ? __ldg(reinterpret_cast<const float4 *>(cube + pix * C) + c4)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][4 * c4] = q.x;
+            v[u][4 * c4 + 1] = q.y;
+            v[u][4 * c4 + 2] = q.z;
+            v[u][4 * c4 + 3] = q.w;
+          }
+          continue;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < CM; ++c) v[u][c] = (c < C && pix < n_pix) ? ldg(cube + pix * C + c) : TIn(0);
     }
@@ -394,7 +408,17 @@ static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const
     dim3 grid((unsigned)nb, (unsigned)n_cubes);
 #define CV_PX(KB, CM) \
   k_pca_project_px<TIn, TO, KB, CM, PPT><<<grid, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err)
-    if (p.C <= 8) {
+    const bool al = ((uintptr_t)src & 15) == 0;
+    if (p.C == 12 && al) {  // e.g. ERA5 / SimpleS2: exact-width register arrays, 16-byte loads,
+                            // one pixel per thread and two CTAs per SM
+      int64_t nb1 = (n_pix + NT - 1) / NT;
+      if (nb1 > 2 * cap) nb1 = 2 * cap;
+      dim3 grid1((unsigned)(nb1 < 1 ? 1 : nb1), (unsigned)n_cubes);
+      if (p.K <= 8)
+        k_pca_project_px<TIn, TO, 8, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+      else
+        k_pca_project_px<TIn, TO, 12, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+    } else if (p.C <= 8) {
       if (p.K <= 8) CV_PX(8, 8); else CV_PX(16, 8);
     } else {
       if (p.K <= 8) CV_PX(8, 16); else CV_PX(16, 16);
