@@ -77,17 +77,24 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
         if (pca) {
           if constexpr (RS == RS_FRAMES_U16) {
             const size_t sm = sizeof(Ssim6SharedT<true>);
-            cudaFuncSetAttribute(k_eval_ssim6<RS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_eval_ssim6<RS, false, true><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
+#define CV_S6P(EP)                                                                                     \
+  do {                                                                                                 \
+    cudaFuncSetAttribute(k_eval_ssim6<RS, false, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_eval_ssim6<RS, false, EP><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);                             \
+  } while (0)
+            if (a.E == 6) CV_S6P(6);
+            else if (a.E == 9) CV_S6P(9);
+            else CV_S6P(k6PcaMax);
+#undef CV_S6P
           }
         } else {
           const size_t sm = sizeof(Ssim6Shared);
           if (a.bit_depth <= 10) {
-            cudaFuncSetAttribute(k_eval_ssim6<RS, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_eval_ssim6<RS, true, false><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
+            cudaFuncSetAttribute(k_eval_ssim6<RS, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_eval_ssim6<RS, true, 0><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
           } else {
-            cudaFuncSetAttribute(k_eval_ssim6<RS, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_eval_ssim6<RS, false, false><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
+            cudaFuncSetAttribute(k_eval_ssim6<RS, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_eval_ssim6<RS, false, 0><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
           }
         }
         return check_launch("cv_eval(ssim6)");

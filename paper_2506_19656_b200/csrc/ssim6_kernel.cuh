@@ -67,6 +67,7 @@ struct Ssim6SharedT {
   // and base_c = mean_c + sum_j min_j W[j][c] (the dequantisation folded into
   // the inverse projection; float64 throughout)
   double coef[PCA ? k6Chans : 1][PCA ? k6PcaMax : 1];
+  int64_t poff[PCA ? k6PcaMax : 1];  // PCA: element offset of plane j from plane 0
   double base[k6Chans];
 };
 using Ssim6Shared = Ssim6SharedT<false>;
@@ -117,9 +118,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity
 
 __host__ __device__ inline int ssim6_groups(int64_t W) { return (int)((W - 2 * kSsimRadius + k6Out - 1) / k6Out); }
 
-template <int RS, bool LUT, bool PCA>
+// EP: 0 without PCA, else the component-plane count the loops are unrolled
+// for (E itself for the common 6 and 9, k6PcaMax with runtime guards otherwise)
+template <int RS, bool LUT, int EP>
 __global__ void __launch_bounds__(256, CVB_SSIM6_MINB)
 k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
+  constexpr bool PCA = EP > 0;
   using R = typename RawT<RS>::type;
   constexpr int FPW = (RS == RS_FRAMES_U8) ? 4 : 2;  // frame samples per 32-bit word
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -142,6 +146,10 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
 
   const int E = args.E;
   if constexpr (PCA) {
+    if (threadIdx.x < E) {
+      const int jp = threadIdx.x;
+      sh.poff[jp] = ((int64_t)(jp / 3) * 3 * args.T + jp % 3) * args.H * args.W;
+    }
     const int cc = cgrp * k6Chans + (int)threadIdx.x / k6PcaMax, jj = (int)threadIdx.x % k6PcaMax;
     if (threadIdx.x < k6Chans * k6PcaMax && cc < C && jj < E) {
       const double m = args.qmins[a * E + jj];
@@ -198,8 +206,9 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   const int xc = vimg ? xv : W32 - 1;  // clamped column: loads stay in bounds
 
   const float *obase = reinterpret_cast<const float *>(args.orig) + (a * T + t) * inner + c;
-  // non-PCA: the band's own plane; PCA: plane (lane >> 4) (lane pairs of planes below)
-  const int fpl = PCA ? (lane >> 4) : c;
+  // non-PCA: the band's own plane; PCA: component plane 0 (+ poff[j] per copy)
+  const int fpl = PCA ? 0 : c;
+  const int Eg = (EP == k6PcaMax) ? E : EP;  // compile-time for the exact-E instances
   const R *fbase = reinterpret_cast<const R *>(args.frames) + (((a * args.G + fpl / 3) * T + t) * 3 + fpl % 3) * HW;
   // frame words: the warp's 32 samples start `foff` samples into the 4-byte word at xa
   const int xw = (int)x0 + 32 * j;
@@ -210,13 +219,7 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   // lanes outside the frame, whose results are never counted)
   const bool fok = PCA ? true : lane < (foff + 32 + FPW - 1) / FPW;
   const int fxc = min(fx, W32 - FPW);  // W % 4 == 0: words never straddle the row end
-  // PCA: copy k of a row moves plane 2k + (lane >> 4), word lane & 15; the
-  // plane offset relative to plane lane >> 4 (planes j: video j/3, slot j%3)
-  auto pdelta = [&](int k) -> int64_t {
-    const int jj = 2 * k + (lane >> 4), j0 = lane >> 4;
-    return ((int64_t)(jj / 3 - j0 / 3) * 3 * T + (jj % 3 - j0 % 3)) * HW;
-  };
-  const int ncopy = (E + 1) / 2;  // PCA copies per lane and row
+  // PCA: copy k of a row moves plane 2k + (lane >> 4), word lane & 15
   const char *ip_o = reinterpret_cast<const char *>(obase + (int64_t)xc * C);
   const char *ip_f = reinterpret_cast<const char *>(fbase + (fok ? fxc : 0));
   const int64_t ostride = rowlen * (int64_t)sizeof(float), fstride = W * (int64_t)sizeof(R);
@@ -226,11 +229,13 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
   auto copy_frames = [&](uint32_t soff) {
     if constexpr (PCA) {
 #pragma unroll
-      for (int k = 0; k < (k6PcaMax + 1) / 2; ++k)
-        if (k < ncopy && (2 * k + (lane >> 4) < E) && fok)
+      for (int k = 0; k < (EP + 1) / 2; ++k) {
+        const int jj = 2 * k + (lane >> 4);
+        if (jj < Eg)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + soff + k * 32 * 4),
-                       "l"(ip_f + pdelta(k) * (int64_t)sizeof(R))
+                       "l"(ip_f + sh.poff[jj] * (int64_t)sizeof(R))
                        : "memory");
+      }
     } else {
       if (fok) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa_f + soff), "l"(ip_f) : "memory");
     }
@@ -277,8 +282,8 @@ k_eval_ssim6(const EvalArgs args, const PcaParams inv) {
       double acc = sh.base[cl];
       q = 0;
 #pragma unroll
-      for (int jj = 0; jj < k6PcaMax; ++jj) {
-        if (jj < E) {
+      for (int jj = 0; jj < EP; ++jj) {
+        if (jj < Eg) {
           const uint32_t qj = (sh.raw_f[w][st][16 * jj + fw] >> fsh) & 0xffffu;
           q = max(q, qj);
           acc = __fma_rn((double)qj, sh.coef[cl][jj], acc);
