@@ -16,7 +16,10 @@
 
 namespace cvb {
 
-constexpr int kQStages = 4;
+#ifndef CVB_QSTAGES
+#define CVB_QSTAGES 4
+#endif
+constexpr int kQStages = CVB_QSTAGES;
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),

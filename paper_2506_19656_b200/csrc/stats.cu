@@ -13,6 +13,10 @@
 #include <type_traits>
 #include "common.cuh"
 
+#ifndef CVB_STATS_KV
+#define CVB_STATS_KV 2  // float4 vectors per thread and time step
+#endif
+
 namespace cvb {
 
 constexpr int kStatsK = 4;
@@ -296,7 +300,7 @@ static void launch_stats(const void *src, int64_t n, int64_t T, int64_t inner, i
   const int NT = threads_for_channels(C);
   const int64_t nseg = (T + seg_len - 1) / seg_len;
   if constexpr (std::is_same<TIn, float>::value || std::is_same<TIn, uint16_t>::value) {
-    constexpr int KV = 2;
+    constexpr int KV = CVB_STATS_KV;
     if (inner % 4 == 0 && (((uintptr_t)src | (uintptr_t)seg_last) & 15) == 0) {
       const int64_t nchunk = (inner + (int64_t)NT * 4 * KV - 1) / ((int64_t)NT * 4 * KV);
       dim3 grid((unsigned)nchunk, (unsigned)nseg, (unsigned)n);
