@@ -379,7 +379,8 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
                      int64_t n_cubes, cudaStream_t st) {
   constexpr int VE = 16 / sizeof(TIn);
   // pixel pairs with register-resident band constants (the common case)
-  const bool px2 = !PCA && args.C <= kQRegC && args.HW % 2 == 0 && !getenv("CVB_QP_PX1");
+  const bool px2 = (PCA ? (args.C <= kQPcaC && args.E <= kQPcaC) : args.C <= kQRegC) && args.HW % 2 == 0 &&
+                   !getenv("CVB_QP_PX1");
   const int NT = px2 ? 128 : 256;
   const int P = px2 ? 2 * NT : NT;
   const int NE = P * args.C;
@@ -394,13 +395,11 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
   } while (0)
-  if constexpr (!PCA) {
-    if (px2) {
-      if (mv <= 2) CV_QP(2, true);
-      else if (mv <= 4) CV_QP(4, true);
-      else CV_QP(8, true);
-      return check_launch("cv_quantize(planar)");
-    }
+  if (px2) {
+    if (mv <= 2) CV_QP(2, true);
+    else if (mv <= 4) CV_QP(4, true);
+    else CV_QP(8, true);
+    return check_launch("cv_quantize(planar)");
   }
   if (mv <= 2) CV_QP(2, false);
   else if (mv <= 4) CV_QP(4, false);

@@ -107,7 +107,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   QBand32 rb[PX2 ? kQRegC : 1];
   const int64_t gjump = (3 * T - 2) * HW;  // plane 2 of video g -> plane 0 of video g+1
   if constexpr (PX2) obase += t0 * 3 * HW;
-  if constexpr (PX2) {
+  if constexpr (PX2 && !PCA) {
 #pragma unroll
     for (int c = 0; c < kQRegC; ++c) rb[c] = qtab32[c < C ? c : 0];
   }
@@ -139,7 +139,46 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
     // refill the stage consumed one step ago (every thread is past it now)
     if (t + kQStages - 1 < t1) issue(t + kQStages - 1);
     cp_async_commit_q();
-    if (PX2 && pvalid) {
+    if (PX2 && PCA && pvalid) {
+      // PCA pixel pair (p, p+1): both projections in registers (two independent
+      // float64 chains), one 32-bit / 16-bit store per component plane
+      const TIn *px = st + p * C;
+      TOut *op = obase + (t - t0) * 3 * HW;
+      using W2 = typename std::conditional<sizeof(TOut) == 1, uint16_t, uint32_t>::type;
+      double d0[kQPcaC], d1[kQPcaC];
+#pragma unroll
+      for (int c = 0; c < kQPcaC; ++c) {
+        d0[c] = c < C ? __dsub_rn((double)px[c], pca.mean[c]) : 0.0;
+        d1[c] = c < C ? __dsub_rn((double)px[C + c], pca.mean[c]) : 0.0;
+      }
+      uint32_t l0 = 0, l1 = 0;
+#pragma unroll
+      for (int pl = 0; pl < 3 * ((kQPcaC + 2) / 3); ++pl) {
+        if (pl < 3 * args.G) {
+          uint32_t q0, q1;
+          if (pl < E) {
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int c = 0; c < kQPcaC; ++c)
+              if (c < C) {
+                a0 = __fma_rn(d0[c], pca.W[pl * kMaxC + c], a0);
+                a1 = __fma_rn(d1[c], pca.W[pl * kMaxC + c], a1);
+              }
+            const QBand b = qtab[pl];
+            q0 = quantize_value(range_prep(a0, b, args.clamp, bad), b);
+            q1 = quantize_value(range_prep(a1, b, args.clamp, bad), b);
+            l0 = q0;
+            l1 = q1;
+          } else {
+            const bool rep = args.pad_mode == CV_PAD_REPEAT;
+            q0 = rep ? l0 : 0u;
+            q1 = rep ? l1 : 0u;
+          }
+          *reinterpret_cast<W2 *>(op) = (W2)(q0 | (q1 << (8 * sizeof(TOut))));
+          op += (pl % 3 == 2) ? gjump : HW;
+        }
+      }
+    } else if (PX2 && !PCA && pvalid) {
       // pixel pair (p, p+1); npix and p are even
       const TIn *px = st + p * C;
       TOut *op = obase + (t - t0) * 3 * HW;  // plane 0 of video 0 at time t
