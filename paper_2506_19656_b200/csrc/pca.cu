@@ -13,7 +13,10 @@
 namespace cvb {
 
 constexpr int kGramK = 4;   // elements per thread per chunk (projection)
-constexpr int kGramKG = 16; // elements per thread per chunk (Gram): 4x the work per barrier
+#ifndef CVB_GRAM_K
+#define CVB_GRAM_K 16
+#endif
+constexpr int kGramKG = CVB_GRAM_K;  // elements per thread per chunk (Gram): 4x the work per barrier
 
 // Gram partial of one CTA over a grid-stride set of pixel chunks.
 // Staging: thread-owns-elements (band tid % C) -> shifted f64 in smem;
