@@ -26,6 +26,7 @@
 #include "ssim_kernel.cuh"
 #include "ssim4_kernel.cuh"
 #include "ssim6_kernel.cuh"
+#include "psnr_kernel.cuh"
 
 #include <cstdlib>
 
@@ -123,6 +124,21 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
       k_eval_ssim<TO, RS, false, false><<<grid, 32 * wpc, 0, st>>>(a, inv);
     }
     return check_launch("cv_eval(ssim)");
+  }
+  if constexpr ((RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) &&
+                (std::is_same<TO, float>::value || std::is_same<TO, uint16_t>::value)) {
+    if (a.psnr_vec) {
+      dim3 gp((unsigned)a.nstrips, (unsigned)a.T, (unsigned)n);
+#define CV_PS(CC)                                                                        \
+  do {                                                                                   \
+    if (a.bit_depth <= 8) k_eval_psnr<TO, RS, true, CC><<<gp, kPsThreads, 0, st>>>(a);  \
+    else k_eval_psnr<TO, RS, false, CC><<<gp, kPsThreads, 0, st>>>(a);                   \
+  } while (0)
+      if (a.C == 4) CV_PS(4);
+      else CV_PS(7);
+#undef CV_PS
+      return check_launch("cv_eval(psnr)");
+    }
   }
   const int NT = a.TX * a.C;
   dim3 grid((unsigned)a.nstrips, (unsigned)a.T, (unsigned)n);
@@ -236,6 +252,15 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, 
   a.ssim6 = ssim && frames && odtype == CV_F32 && W % 4 == 0 && !getenv("CVB_SSIM_V5") &&
             (!pca || (fdtype == CV_U16 && E <= k6PcaMax));
   if (a.ssim6) a.nstrips = 4 * ssim6_groups(W);
+  // streaming PSNR-only kernel: frames, f32/u16 original, no PCA, C in {4, 7},
+  // 4-pixel quads; nstrips = pixel chunks per frame (<= the workspace's strips)
+  a.psnr_vec = !ssim && frames && !pca && (odtype == CV_F32 || odtype == CV_U16) && (C == 4 || C == 7) &&
+               (H * W) % 4 == 0 && !getenv("CVB_PSNR_ROWS");
+  if (a.psnr_vec) {
+    const int64_t want = (H * W + 32767) / 32768;  // ~32 K pixels per CTA
+    a.nstrips = (int)(want < a.nstrips ? want : a.nstrips);
+    if (a.nstrips < 1) a.nstrips = 1;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int s;
   switch (odtype) {

@@ -36,6 +36,7 @@ struct EvalArgs {
   uint32_t *err;
   int TX, nstrips;
   int ssim6;  // launch k_eval_ssim6 (nstrips = 4 * ssim6_groups(W))
+  int psnr_vec;  // launch k_eval_psnr (nstrips = pixel chunks per frame)
 };
 
 enum { RS_FRAMES_U8 = 0, RS_FRAMES_U16 = 1, RS_RECON_F32 = 2, RS_RECON_F64 = 3 };

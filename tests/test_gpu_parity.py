@@ -346,3 +346,24 @@ def test_ssim_column_groups(cuda, shape, B):
     rep = sc.report()[0]
     np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), rtol=1e-9)
     np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
+
+
+@pytest.mark.parametrize("shape,B,u16", [((5, 16, 20, 7), 12, False), ((3, 40, 36, 4), 16, False),
+                                         ((4, 24, 28, 4), 8, True), ((2, 13, 12, 7), 10, True)])
+def test_psnr_stream_kernel(cuda, shape, B, u16):
+    """PSNR-only decode (streaming kernel for C in {4, 7}, H*W % 4 == 0): recon
+    bit-exact and per-band PSNR against the oracle, f32 and u16 originals,
+    table and computed dequantisation."""
+    rng = np.random.default_rng(sum(shape) + B)
+    if u16:
+        x = rng.integers(0, 10001, size=shape).astype(np.uint16)
+    else:
+        x = (rng.random(shape) * 2 + 0.5).astype(np.float32)
+        x[rng.random(shape) < 0.05] = np.nan
+    enc, recon, sc = G_pipe.roundtrip(torch.from_numpy(x).to(cuda), G_pipe.StreamSpec(B), want_ssim=False)
+    enc.check()
+    ref = O.encode_stream(x, B)
+    rec_o = O.decode_stream(ref["frames"], ref, x.shape, B)
+    np.testing.assert_array_equal(recon.cpu().numpy(), rec_o.astype(np.float32))
+    rep = sc.report()[0]
+    np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), rtol=1e-9)
