@@ -164,6 +164,174 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
   }
 }
 
+// Pixel-per-lane Gram for float32 cubes with C <= kGpxC (ERA5 / SimpleS2: 12).
+// Chunks of kGpxP pixels stream through a kGpxS-stage cp.async ring (one CTA
+// per SM, ~30 KB in flight). Warp pair (2g, 2g+1) takes pixels g*32 + lane of
+// the chunk; warp parity H owns half of the C(C+1)/2 products (static register
+// indices, no shared-memory tiles) and the band statistics of bands
+// [H*kGpxC/2, (H+1)*kGpxC/2). Same shifted one-pass sums as k_gram (shift =
+// the first pixel), deterministic fixed-order reductions.
+constexpr int kGpxC = 12;
+constexpr int kGpxP = 128;
+constexpr int kGpxS = 6;
+constexpr int kGpxNP = kGpxC * (kGpxC + 1) / 2;  // 78 products
+constexpr int kGpxHalf = kGpxNP / 2;              // 39 per warp parity
+
+__device__ __forceinline__ void gram_cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+template <int H>
+__device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px, int C, const float (&sh)[kGpxC],
+                                                   double (&acc)[kGpxHalf], double (&bsum)[kGpxC / 2],
+                                                   float (&mn)[kGpxC / 2], float (&mx)[kGpxC / 2], bool &isn,
+                                                   bool &nonfinite) {
+  float x[kGpxC];
+  if (C == kGpxC) {
+#pragma unroll
+    for (int q = 0; q < kGpxC / 4; ++q) {
+      const float4 v = *reinterpret_cast<const float4 *>(px + 4 * q);
+      x[4 * q] = v.x, x[4 * q + 1] = v.y, x[4 * q + 2] = v.z, x[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < kGpxC; ++c) x[c] = c < C ? px[c] : sh[c];
+  }
+  double d[kGpxC];
+#pragma unroll
+  for (int c = 0; c < kGpxC; ++c) {
+    const double dd = __dsub_rn((double)x[c], (double)sh[c]);
+    d[c] = isfinite(dd) ? dd : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < kGpxC / 2; ++j) {
+    const int c = H * (kGpxC / 2) + j;
+    if (c < C) {
+      const float v = x[c];
+      isn |= isnan(v);
+      nonfinite |= isinf(v);
+      mn[j] = fminf(mn[j], v);
+      mx[j] = fmaxf(mx[j], v);
+      bsum[j] = __dadd_rn(bsum[j], d[c]);
+    }
+  }
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < kGpxC; ++i)
+#pragma unroll
+    for (int j = i; j < kGpxC; ++j, ++k)
+      if (k >= H * kGpxHalf && k < (H + 1) * kGpxHalf) acc[k - H * kGpxHalf] = __fma_rn(d[i], d[j], acc[k - H * kGpxHalf]);
+}
+
+__global__ void __launch_bounds__(256, 1)
+k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restrict__ partials,
+          StatsEntry *__restrict__ stats, uint32_t *err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float *ring = reinterpret_cast<float *>(smem);  // [kGpxS][kGpxP * C]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int H = warp & 1, wg = warp >> 1;
+  const int SE = kGpxP * C;
+  const int nvec = SE / 4;
+  const int64_t ne = n_pix * C;
+  const int64_t nchunks = (n_pix + kGpxP - 1) / kGpxP;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t nit = b < nchunks ? (nchunks - b + G - 1) / G : 0;
+
+  float sh[kGpxC];
+#pragma unroll
+  for (int c = 0; c < kGpxC; ++c) sh[c] = c < C ? ldg(src + c) : 0.f;
+
+  auto issue = [&](int64_t it) {
+    float *st = ring + (size_t)(it % kGpxS) * SE;
+    const int64_t e0 = (b + it * G) * SE;
+    for (int v = tid; v < nvec; v += blockDim.x) {
+      const int64_t e = e0 + 4 * (int64_t)v;
+      if (e + 4 <= ne) gram_cp_async16(st + 4 * v, src + e);
+      else
+        for (int j = 0; j < 4; ++j) st[4 * v + j] = e + j < ne ? src[e + j] : 0.f;
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < kGpxS - 1; ++s) {
+    if (s < nit) issue(s);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+
+  double acc[kGpxHalf];
+#pragma unroll
+  for (int k = 0; k < kGpxHalf; ++k) acc[k] = 0.0;
+  double bsum[kGpxC / 2];
+  float mn[kGpxC / 2], mx[kGpxC / 2];
+#pragma unroll
+  for (int j = 0; j < kGpxC / 2; ++j) bsum[j] = 0.0, mn[j] = INFINITY, mx[j] = -INFINITY;
+  bool isn = false, nonfinite = false;
+  const int p = wg * 32 + lane;
+
+  for (int64_t it = 0; it < nit; ++it) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kGpxS - 2) : "memory");
+    __syncthreads();
+    if (it + kGpxS - 1 < nit) issue(it + kGpxS - 1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const float *st = ring + (size_t)(it % kGpxS) * SE;
+    if ((b + it * G) * kGpxP + p < n_pix) {
+      if (H == 0) gram_px_accumulate<0>(st + p * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+      else gram_px_accumulate<1>(st + p * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  flag_warp(err, nonfinite, CV_FLAG_NONFINITE);
+  flag_warp(err, isn, CV_FLAG_NAN);
+
+  // warp butterflies (fixed order), then the 4 pixel groups summed in order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < kGpxHalf; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+#pragma unroll
+    for (int j = 0; j < kGpxC / 2; ++j) {
+      bsum[j] += __shfl_xor_sync(0xffffffffu, bsum[j], o);
+      mn[j] = fminf(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
+      mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
+    }
+  }
+  __syncthreads();  // ring reused as the reduction buffer
+  double *red = reinterpret_cast<double *>(smem);  // [4][kGpxNP + kGpxC]
+  constexpr int RS = kGpxNP + kGpxC;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kGpxHalf; ++k) red[wg * RS + H * kGpxHalf + k] = acc[k];
+#pragma unroll
+    for (int j = 0; j < kGpxC / 2; ++j) {
+      const int c = H * (kGpxC / 2) + j;
+      red[wg * RS + kGpxNP + c] = bsum[j];
+      if (stats && c < C && mn[j] <= mx[j]) {
+        atomicMin(&stats[c].min_key, dkey((double)mn[j]));
+        atomicMax(&stats[c].max_key, dkey((double)mx[j]));
+      }
+    }
+  }
+  __syncthreads();
+  double *part = partials + (size_t)b * (C + C * C);
+  const int ngroups = blockDim.x / 64;
+  for (int idx = tid; idx < RS; idx += blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < ngroups; ++g) s += red[g * RS + idx];
+    if (idx < kGpxNP) {
+      int i = 0, rem = idx;
+      while (rem >= kGpxC - i) rem -= kGpxC - i, ++i;
+      const int j = i + rem;
+      if (i < C && j < C) {
+        part[C + i * C + j] = s;
+        part[C + j * C + i] = s;
+      }
+    } else if (idx - kGpxNP < C) {
+      part[idx - kGpxNP] = s;
+    }
+  }
+}
+
 __global__ void k_reduce_partials(const double *__restrict__ partials, int nparts, int stride,
                                   double *__restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -380,6 +548,22 @@ static int gram_blocks(int64_t n_pix, int C) {
 template <typename TIn>
 static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *out, void *stats,
                        uint32_t *err, cudaStream_t st) {
+  if constexpr (std::is_same<TIn, float>::value) {
+    if (C <= kGpxC && ((uintptr_t)src & 15) == 0 && !getenv("CVB_GRAM_TILES")) {
+      int nblk = gram_blocks(n_pix, C);
+      if (nblk > num_sms()) nblk = num_sms();
+      size_t sm = (size_t)kGpxS * kGpxP * C * sizeof(float);
+      const size_t smr = (size_t)4 * (kGpxNP + kGpxC) * sizeof(double);
+      if (smr > sm) sm = smr;
+      if (sm > 48 * 1024) cudaFuncSetAttribute(k_gram_px, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_gram_px<<<nblk, 256, sm, st>>>((const float *)src, n_pix, C, (double *)ws, (StatsEntry *)stats, err);
+      int s = check_launch("cv_pca_gram(px)");
+      if (s != CV_OK) return s;
+      const int stride = C + C * C;
+      k_reduce_partials<<<(stride + 255) / 256, 256, 0, st>>>((const double *)ws, nblk, stride, out);
+      return check_launch("cv_pca_gram(reduce)");
+    }
+  }
   const int NT = threads_for_channels(C);
   const int P = NT * kGramKG / C;
   const int nb = (C + 3) / 4, ntile = nb * (nb + 1) / 2;
