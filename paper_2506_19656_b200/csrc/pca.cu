@@ -166,13 +166,13 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
 
 // Pixel-per-lane Gram for float32 cubes with C <= kGpxC (ERA5 / SimpleS2: 12).
 // Chunks of kGpxP pixels stream through a kGpxS-stage cp.async ring (one CTA
-// per SM, ~30 KB in flight). Warp pair (2g, 2g+1) takes pixels g*32 + lane of
+// per SM, ~60 KB in flight). Warp pair (2g, 2g+1) takes pixels g*32 + lane (+128) of
 // the chunk; warp parity H owns half of the C(C+1)/2 products (static register
 // indices, no shared-memory tiles) and the band statistics of bands
 // [H*kGpxC/2, (H+1)*kGpxC/2). Same shifted one-pass sums as k_gram (shift =
 // the first pixel), deterministic fixed-order reductions.
 constexpr int kGpxC = 12;
-constexpr int kGpxP = 128;
+constexpr int kGpxP = 256;  // two pixels per thread per chunk
 constexpr int kGpxS = 6;
 constexpr int kGpxNP = kGpxC * (kGpxC + 1) / 2;  // 78 products
 constexpr int kGpxHalf = kGpxNP / 2;              // 39 per warp parity
@@ -275,9 +275,13 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
     if (it + kGpxS - 1 < nit) issue(it + kGpxS - 1);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     const float *st = ring + (size_t)(it % kGpxS) * SE;
-    if ((b + it * G) * kGpxP + p < n_pix) {
-      if (H == 0) gram_px_accumulate<0>(st + p * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
-      else gram_px_accumulate<1>(st + p * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+#pragma unroll
+    for (int r = 0; r < kGpxP / 128; ++r) {
+      const int pp = p + 128 * r;
+      if ((b + it * G) * kGpxP + pp < n_pix) {
+        if (H == 0) gram_px_accumulate<0>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+        else gram_px_accumulate<1>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+      }
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
