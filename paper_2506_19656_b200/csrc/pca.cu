@@ -172,7 +172,7 @@ k_gram(const TIn *__restrict__ src, int64_t n_pix, int C, double *__restrict__ p
 // [H*kGpxC/2, (H+1)*kGpxC/2). Same shifted one-pass sums as k_gram (shift =
 // the first pixel), deterministic fixed-order reductions.
 constexpr int kGpxC = 12;
-constexpr int kGpxP = 256;  // two pixels per thread per chunk
+constexpr int kGpxR = 2;  // pixel rounds per chunk: a chunk is blockDim.x pixels
 constexpr int kGpxS = 6;
 constexpr int kGpxNP = kGpxC * (kGpxC + 1) / 2;  // 78 products
 constexpr int kGpxHalf = kGpxNP / 2;              // 39 per warp parity
@@ -225,10 +225,12 @@ __device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px,
       if (k >= H * kGpxHalf && k < (H + 1) * kGpxHalf) acc[k - H * kGpxHalf] = __fma_rn(d[i], d[j], acc[k - H * kGpxHalf]);
 }
 
-__global__ void __launch_bounds__(256, 1)
+template <int NT>
+__global__ void __launch_bounds__(NT, NT <= 64 ? 5 : 1)
 k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restrict__ partials,
           StatsEntry *__restrict__ stats, uint32_t *err) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int kGpxP = NT;  // pixels per chunk
   float *ring = reinterpret_cast<float *>(smem);  // [kGpxS][kGpxP * C]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = warp & 1, wg = warp >> 1;
@@ -246,7 +248,7 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
   auto issue = [&](int64_t it) {
     float *st = ring + (size_t)(it % kGpxS) * SE;
     const int64_t e0 = (b + it * G) * SE;
-    for (int v = tid; v < nvec; v += blockDim.x) {
+    for (int v = tid; v < nvec; v += NT) {
       const int64_t e = e0 + 4 * (int64_t)v;
       if (e + 4 <= ne) gram_cp_async16(st + 4 * v, src + e);
       else
@@ -276,8 +278,8 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     const float *st = ring + (size_t)(it % kGpxS) * SE;
 #pragma unroll
-    for (int r = 0; r < kGpxP / 128; ++r) {
-      const int pp = p + 128 * r;
+    for (int r = 0; r < kGpxR; ++r) {
+      const int pp = p + (NT / 2) * r;
       if ((b + it * G) * kGpxP + pp < n_pix) {
         if (H == 0) gram_px_accumulate<0>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
         else gram_px_accumulate<1>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
@@ -318,7 +320,7 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
   }
   __syncthreads();
   double *part = partials + (size_t)b * (C + C * C);
-  const int ngroups = blockDim.x / 64;
+  constexpr int ngroups = NT / 64;
   for (int idx = tid; idx < RS; idx += blockDim.x) {
     double s = 0.0;
     for (int g = 0; g < ngroups; ++g) s += red[g * RS + idx];
@@ -543,7 +545,7 @@ static int gram_blocks(int64_t n_pix, int C) {
   const int NT = threads_for_channels(C);
   const int P = NT * kGramKG / C;
   const int64_t nchunks = (n_pix + P - 1) / P;
-  int64_t nb = 4 * (int64_t)num_sms();
+  int64_t nb = 5 * (int64_t)num_sms();
   if (nb > nchunks) nb = nchunks;
   if (nb < 1) nb = 1;
   return (int)nb;
@@ -556,11 +558,15 @@ static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *
     if (C <= kGpxC && ((uintptr_t)src & 15) == 0 && !getenv("CVB_GRAM_TILES")) {
       int nblk = gram_blocks(n_pix, C);
       if (nblk > num_sms()) nblk = num_sms();
-      size_t sm = (size_t)kGpxS * kGpxP * C * sizeof(float);
-      const size_t smr = (size_t)4 * (kGpxNP + kGpxC) * sizeof(double);
+      const char *ntv = getenv("CVB_GRAM_NT");
+      const int NT = ntv ? atoi(ntv) : 64;
+      if (NT == 64) nblk = (int)min((int64_t)gram_blocks(n_pix, C), (int64_t)5 * num_sms());
+      size_t sm = (size_t)kGpxS * NT * C * sizeof(float);
+      const size_t smr = (size_t)(NT / 64) * (kGpxNP + kGpxC) * sizeof(double);
       if (smr > sm) sm = smr;
-      if (sm > 48 * 1024) cudaFuncSetAttribute(k_gram_px, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_gram_px<<<nblk, 256, sm, st>>>((const float *)src, n_pix, C, (double *)ws, (StatsEntry *)stats, err);
+      auto kern = NT == 64 ? k_gram_px<64> : k_gram_px<256>;
+      if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<nblk, NT == 64 ? 64 : 256, sm, st>>>((const float *)src, n_pix, C, (double *)ws, (StatsEntry *)stats, err);
       int s = check_launch("cv_pca_gram(px)");
       if (s != CV_OK) return s;
       const int stride = C + C * C;
