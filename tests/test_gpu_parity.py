@@ -367,3 +367,32 @@ def test_psnr_stream_kernel(cuda, shape, B, u16):
     np.testing.assert_array_equal(recon.cpu().numpy(), rec_o.astype(np.float32))
     rep = sc.report()[0]
     np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), rtol=1e-9)
+
+
+# ------------------------------------------------------------------ Gram kernels
+
+@pytest.mark.parametrize("C", [1, 5, 7, 12])
+@pytest.mark.parametrize("n_pix", [1, 63, 64 * 5 + 3, 100_003])
+@pytest.mark.parametrize("variant", [{}, {"CVB_GRAM_NT": "256"}, {"CVB_GRAM_TILES": "1"}])
+def test_gram_kernels_ragged(cuda, monkeypatch, C, n_pix, variant):
+    """k_gram_px (64- and 256-thread CTAs) and the tiled k_gram against a float64
+    numpy shifted Gram (transform.py:177-179 restated as one-pass sums): ragged
+    pixel counts, C below the 12-band register width; band extremes bit-exact."""
+    from paper_2506_19656_b200 import _device as dev
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(1000 * C + n_pix % 997)
+    x = (rng.standard_normal((n_pix, C)) * 10.0 ** np.arange(C) / 7 + 3.0).astype(np.float32)
+    arr = dev.to_device(x)
+    g = G.gram(arr, n_pix, C, stats=True)
+    torch.cuda.synchronize()
+    assert g["err"].flags() == 0
+    out = g["out"].cpu().numpy()
+    d = x.astype(np.float64) - x[0].astype(np.float64)
+    want_sums = d.sum(axis=0)
+    want_G = d.T @ d
+    scale = np.sqrt(np.outer(np.diag(want_G), np.diag(want_G))) + 1e-300
+    np.testing.assert_allclose(out[:C], want_sums, rtol=0, atol=1e-10 * np.abs(d).sum(axis=0).max() + 1e-300)
+    assert np.all(np.abs(out[C:].reshape(C, C) - want_G) <= 1e-10 * scale + 1e-300)
+    np.testing.assert_array_equal(g["mins"].cpu().numpy(), x.min(axis=0).astype(np.float64))
+    np.testing.assert_array_equal(g["maxs"].cpu().numpy(), x.max(axis=0).astype(np.float64))
