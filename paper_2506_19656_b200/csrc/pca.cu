@@ -430,7 +430,7 @@ k_pca_project(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
 template <typename TIn, typename TO, int KB, int CM, int PPT>
 __global__ void __launch_bounds__(256, (CM <= 12 && KB <= 8) ? 2 : 1)
 k_pca_project_px(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
-                 StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err) {
+                 StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err, bool pca_px_noprefetch = false) {
   const int C = pca.C, K = pca.K;
   const int64_t a = blockIdx.y;
   const TIn *cube = src + a * n_pix * C;
@@ -442,7 +442,50 @@ k_pca_project_px(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ ou
   }
   bool bad = false;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * PPT;
-  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x * PPT + threadIdx.x; p0 < n_pix; p0 += stride) {
+  bool done = false;
+  if constexpr (std::is_same<TIn, float>::value && CM % 4 == 0 && PPT == 1) {
+    if (C == CM && !pca_px_noprefetch) {
+      // exact-width pixels, software-pipelined: the next pixel's CM/4 16-byte
+      // loads are in flight while this one is projected
+      auto load = [&](int64_t pix, float4 (&q)[CM / 4]) {
+#pragma unroll
+        for (int c4 = 0; c4 < CM / 4; ++c4)
+          q[c4] = pix < n_pix ? __ldg(reinterpret_cast<const float4 *>(cube + pix * C) + c4)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      float4 nq[CM / 4];
+      int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+      load(pix, nq);
+      for (; pix < n_pix; pix += stride) {
+        float xv[CM];
+#pragma unroll
+        for (int c4 = 0; c4 < CM / 4; ++c4) {
+          xv[4 * c4] = nq[c4].x, xv[4 * c4 + 1] = nq[c4].y, xv[4 * c4 + 2] = nq[c4].z, xv[4 * c4 + 3] = nq[c4].w;
+        }
+        load(pix + stride, nq);
+        double d[CM];
+#pragma unroll
+        for (int c = 0; c < CM; ++c) {
+          const double x = (double)xv[c];
+          bad |= !isfinite(x);
+          d[c] = __dsub_rn(x, pca.mean[c]);
+        }
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+          if (j < K) {
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < CM; ++c) acc = __fma_rn(d[c], pca.W[j * kMaxC + c], acc);
+            mn[j] = fmin(mn[j], acc);
+            mx[j] = fmax(mx[j], acc);
+            if (out) out[(a * n_pix + pix) * K + j] = (TO)acc;
+          }
+        }
+      }
+      done = true;
+    }
+  }
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x * PPT + threadIdx.x; !done && p0 < n_pix; p0 += stride) {
     TIn v[PPT][CM];
 #pragma unroll
     for (int u = 0; u < PPT; ++u) {
@@ -612,9 +655,9 @@ static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const
       if (nb1 > 2 * cap) nb1 = 2 * cap;
       dim3 grid1((unsigned)(nb1 < 1 ? 1 : nb1), (unsigned)n_cubes);
       if (p.K <= 8)
-        k_pca_project_px<TIn, TO, 8, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+        k_pca_project_px<TIn, TO, 8, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err, getenv("CVB_PROJ_NOPF") != nullptr);
       else
-        k_pca_project_px<TIn, TO, 12, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+        k_pca_project_px<TIn, TO, 12, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err, getenv("CVB_PROJ_NOPF") != nullptr);
     } else if (p.C <= 8) {
       if (p.K <= 8) CV_PX(8, 8); else CV_PX(16, 8);
     } else {
