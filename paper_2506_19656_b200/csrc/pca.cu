@@ -338,13 +338,18 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
   }
 }
 
+// one warp per output: lanes stride over the CTA partials, fixed butterfly
+// (deterministic for a given grid)
 __global__ void k_reduce_partials(const double *__restrict__ partials, int nparts, int stride,
                                   double *__restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
   if (i >= stride) return;
   double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += partials[(size_t)p * stride + i];
-  out[i] = s;
+  for (int p = lane; p < nparts; p += 32) s += partials[(size_t)p * stride + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[i] = s;
 }
 
 // Projection: stage spectra (thread-owns-elements), then one thread per pixel
@@ -613,7 +618,7 @@ static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *
       int s = check_launch("cv_pca_gram(px)");
       if (s != CV_OK) return s;
       const int stride = C + C * C;
-      k_reduce_partials<<<(stride + 255) / 256, 256, 0, st>>>((const double *)ws, nblk, stride, out);
+      k_reduce_partials<<<(stride + 7) / 8, 256, 0, st>>>((const double *)ws, nblk, stride, out);
       return check_launch("cv_pca_gram(reduce)");
     }
   }
@@ -631,7 +636,7 @@ static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *
   int s = check_launch("cv_pca_gram");
   if (s != CV_OK) return s;
   const int stride = C + C * C;
-  k_reduce_partials<<<(stride + 255) / 256, 256, 0, st>>>((const double *)ws, nblk, stride, out);
+  k_reduce_partials<<<(stride + 7) / 8, 256, 0, st>>>((const double *)ws, nblk, stride, out);
   return check_launch("cv_pca_gram(reduce)");
 }
 
