@@ -183,11 +183,12 @@ __device__ __forceinline__ void gram_cp_async16(void *dst, const void *src) {
                : "memory");
 }
 
-template <int H>
-__device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px, int C, const float (&sh)[kGpxC],
+template <int H, bool EXACT>
+__device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px, int C_, const float (&sh)[kGpxC],
                                                    double (&acc)[kGpxHalf], double (&bsum)[kGpxC / 2],
                                                    float (&mn)[kGpxC / 2], float (&mx)[kGpxC / 2], bool &isn,
                                                    bool &nonfinite) {
+  const int C = EXACT ? kGpxC : C_;
   float x[kGpxC];
   if (C == kGpxC) {
 #pragma unroll
@@ -281,8 +282,13 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
     for (int r = 0; r < kGpxR; ++r) {
       const int pp = p + (NT / 2) * r;
       if ((b + it * G) * kGpxP + pp < n_pix) {
-        if (H == 0) gram_px_accumulate<0>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
-        else gram_px_accumulate<1>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+        if (C == kGpxC) {
+          if (H == 0) gram_px_accumulate<0, true>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+          else gram_px_accumulate<1, true>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+        } else {
+          if (H == 0) gram_px_accumulate<0, false>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+          else gram_px_accumulate<1, false>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+        }
       }
     }
   }
