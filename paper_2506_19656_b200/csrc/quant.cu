@@ -395,6 +395,12 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
   } while (0)
+  if (px2 && PCA && args.C == 12 && mv <= 8 && mv > 4 && !getenv("CVB_QP_RUNTIME_C")) {
+    auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, 8, true, 12>;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);
+    return check_launch("cv_quantize(planar)");
+  }
   if (px2) {
     if (mv <= 2) CV_QP(2, true);
     else if (mv <= 4) CV_QP(4, true);

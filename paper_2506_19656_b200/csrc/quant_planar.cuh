@@ -38,14 +38,14 @@ __device__ __forceinline__ void cp_async_wait_q() {
 constexpr int kQRegC = 8;
 constexpr int kQPcaC = 16;  // PCA register path: channels and components
 
-template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false>
+template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false, int CX = 0>
 __global__ void __launch_bounds__(256)
 k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs args,
                   const PcaParams pca) {
   constexpr int VE = 16 / sizeof(TIn);  // elements per 16-byte copy
   extern __shared__ __align__(16) unsigned char smem[];
   const int NT = blockDim.x, tid = threadIdx.x;
-  const int C = args.C, E = args.E;
+  const int C = CX ? CX : args.C, E = args.E;  // CX: compile-time band count (PCA, C = 12)
   const int64_t T = args.T, HW = args.HW, inner = HW * C;
   const int P = PX2 ? 2 * NT : NT;          // pixels per chunk
   const int NE = P * C;                     // elements per full chunk
