@@ -1,21 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the B200 array path on BASELINE.json's headline workload.
 
-Default workload (BASELINE.json configs[1], "config 2"): per GPU a batch of 64
-DeepExtremeCubes-shaped minicubes, float32 [495,128,128,7] with 20% NaN frames
-and 2% NaN pixels; one step = forward fill + per-band stats -> 10-bit
-quantisation into planar 3-channel frames -> decode (dequantise) -> per-band
-PSNR + 11x11 Gaussian SSIM, all cubes, inputs resident in HBM. Multi-GPU:
-one process per GPU (torchrun), each rank owns its own 64 cubes (independent
-objects: no data-path collective, weak scaling); step time = max over ranks.
+Default workload: config 5, the ERA5-shaped cube (float32 [744,721,1440,12]),
+the largest single-GPU configuration and the cube `north_star` names for
+scaling. One step = per-band statistics + normalisation -> float64 Gram ->
+host eigh -> PCA 12->6 projection + per-PC ranges -> 16-bit planar frames ->
+decode (dequantise + inverse PCA + de-normalise) -> per-band PSNR + 11x11
+Gaussian SSIM, with the cube resident in HBM. Multi-GPU: one process per GPU,
+the cube sharded along time; the per-band statistics, the C x C Gram partials,
+the PC ranges and the metric sums are combined over NCCL
+(paper_2506_19656_b200.dist). `--config 2` runs 64 DeepExtremeCubes
+minicubes per GPU (weak scaling, no data-path collective); `--config 1/3/4`
+the other BASELINE configurations.
 
-``--config 5`` (ERA5-shaped [744,721,1440,12], normalise + PCA 12->6, 16-bit,
-PSNR+SSIM) and ``--config 1/3/4`` run one cube sharded along time across the
-ranks with the NCCL combines of paper_2506_19656_b200.dist (strong scaling).
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 5]
+
+With --gpus N > 1 and no torchrun environment the script re-launches itself
+under `torch.distributed.run` (one rank per GPU, NCCL, 127.0.0.1).
 
 Metric: Gpixel*band/s (elements of the T*H*W*C cubes per second), whole job.
-
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2]
 """
 
 from __future__ import annotations
@@ -23,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -37,22 +41,45 @@ METRIC = "Gpixel·band/s encode-prep+decode+PSNR/SSIM"
 UNIT = "Gpixel·band/s"
 SEED0 = 19656
 SHAPE2 = (495, 128, 128, 7)
-ELEM2 = SHAPE2[0] * SHAPE2[1] * SHAPE2[2] * SHAPE2[3]
 
 
-def _args():
+def _args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--cubes", type=int, default=64, help="config 2: cubes per GPU (64)")
     ap.add_argument("--t", type=int, default=None, help="override T (time-sharded configs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / CPU arm)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+# ------------------------------------------------------------------------------ launcher
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _maybe_spawn(a) -> int | None:
+    """--gpus N without a torchrun environment: re-launch under torch.distributed.run."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != a.gpus:
+            print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            return 2
+        return None
+    if a.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------------------ workloads
@@ -70,9 +97,11 @@ class Workload:
         self.bit_depth = c["bit_depth"]
         self.n_pcs = c["n_pcs"]
         self.normalize = c.get("normalize", False)
+        self.dtype = c["dtype"]
         if cfg == 2:
             self.cubes = cubes
             self.shape = SHAPE2
+            self.t0 = 0
             self.t_local = SHAPE2[0]
             self.t_total = SHAPE2[0]
             self.sharded = False
@@ -88,24 +117,22 @@ class Workload:
         T, H, W, C = self.shape
         self.elem_rank = self.cubes * self.t_local * H * W * C
         self.elem_total = (self.cubes * world if cfg == 2 else 1) * self.t_total * H * W * C
-        s = 2 if c["dtype"] == "u16" else 4
+        s = 2 if self.dtype == "u16" else 4
         b = 1 if self.bit_depth == 8 else 2
         E = self.n_pcs or C
         P = 3 * ((E + 2) // 3)
         R = 3 if self.n_pcs else 2
-        # SURVEY.md §8d algorithmic bytes per element
+        # SURVEY.md §8d algorithmic bytes per element: enc = R*s + b*P/C,
+        # dec = b*E/C + 4, met = s + 4 (stats / quantise / decode+metrics phases)
         self.alg = {"stats": (R - 1) * s, "quantize": s + b * P / C, "eval": b * E / C + 4 + s + 4}
         self.alg_total = sum(self.alg.values())
-        self.fill = c["dtype"] == "f32" and c.get("nan", False)
 
     def spec(self):
         from paper_2506_19656_b200 import pipeline
 
         return pipeline.StreamSpec(self.bit_depth, n_pcs=self.n_pcs, normalize=self.normalize)
 
-    def make_input(self, dev, rank):
-        import torch
-
+    def make_input(self, dev, rank, device_out=None):
         from paper_2506_19656_b200 import synth
 
         T, H, W, C = self.shape
@@ -118,8 +145,7 @@ class Workload:
             return synth.minicube(synth.SEEDS[1] + 1000 * rank, local, device=dev)
         if self.cfg == 3:
             return synth.simple_s2(synth.SEEDS[3] + 1000 * rank, local, device=dev)
-        x = synth.dynamic_earthnet(synth.SEEDS[4] + 1000 * rank, local, device=dev)
-        return x.contiguous() if isinstance(x, torch.Tensor) else x
+        return synth.dynamic_earthnet(synth.SEEDS[4] + 1000 * rank, local, device=dev).contiguous()
 
     def config_json(self, world):
         T, H, W, C = self.shape
@@ -129,15 +155,17 @@ class Workload:
                     "dequantise, per-band PSNR + 11x11 Gaussian SSIM")
             par = "cube-sharded, one process per GPU, no data-path collective"
         else:
-            work = (f"config{self.cfg}: {self.name} [{T},{H},{W},{C}], {self.bit_depth}-bit"
+            work = (f"config{self.cfg}: {self.name} [{T},{H},{W},{C}] {self.dtype}, {self.bit_depth}-bit"
                     + (f", PCA {C}->{self.n_pcs}" if self.n_pcs else "")
-                    + (" (normalised)" if self.normalize else "")
-                    + (", PSNR + 11x11 SSIM" if self.ssim else ", PSNR"))
-            par = f"time-sharded over {world} GPU(s); NCCL all-reduce/all-gather of stats, Gram, metric sums"
+                    + (" on per-band min/max normalised bands" if self.normalize else "")
+                    + (", PSNR + 11x11 Gaussian SSIM" if self.ssim else ", PSNR"))
+            par = (f"time-sharded over {world} GPU(s), {self.t_local} frames per GPU; NCCL all-reduce/"
+                   "all-gather of band stats, Gram partials, PC ranges, metric sums" if world > 1
+                   else "one GPU")
+        s = 2 if self.dtype == "u16" else 4
         return {"workload": work, "cubes_per_gpu": self.cubes, "elements_per_gpu": self.elem_rank,
                 "bit_depth": self.bit_depth,
-                "l2": f"inputs {self.elem_rank * (2 if self.cfg == 4 else 4) / 1e9:.1f} GB per GPU >> 126 MB "
-                      "L2 (no flush needed)",
+                "l2": f"inputs {self.elem_rank * s / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush needed)",
                 "parallelism": par}
 
 
@@ -215,58 +243,100 @@ def _peaks():
 
 
 # ------------------------------------------------------------------------------ CPU arm
+#
+# The reference's algorithm for this path is cubevid's numpy functions
+# (transform.py / cube.py / plan.py / bridge.py) plus the restated metrics
+# (SPEC.md:412-436). It is a Python package: there is no C/C++ to build into
+# oracle/_ref, and /root/reference is absent on the GPU box, so the CPU arm
+# runs the oracle port of those functions (oracle/, pinned to the reference's
+# own outputs in tests/golden). Workers are independent processes, one per
+# host core; each holds its own sample of the workload (below).
 
-def _cpu_worker(x):
-    """One cube through the oracle port (numpy), fill -> stats -> quantise ->
-    planar frames -> dequantise -> PSNR + SSIM. Returns (elements, seconds)."""
+_SAMPLE = {}
+
+
+def _sample_shape(cfg: int):
+    """Bounded per-worker sample of each configuration (full H x W x C)."""
+    return {1: (124, 128, 128, 7), 2: (124, 128, 128, 7), 3: (4, 512, 512, 12),
+            4: (8, 1024, 1024, 4), 5: (1, 721, 1440, 12)}[cfg]
+
+
+def _cpu_init(cfg: int, counter):
+    import numpy as np  # noqa: F401
+    import torch
+
+    torch.set_num_threads(1)
+    from paper_2506_19656_b200 import synth
+
+    with counter.get_lock():
+        idx = counter.value
+        counter.value += 1
+    shp = _sample_shape(cfg)
+    if cfg in (1, 2):
+        x = synth.minicube(SEED0 + idx, shp)
+    elif cfg == 3:
+        x = synth.simple_s2(synth.SEEDS[3] + idx, shp)
+    elif cfg == 4:
+        x = synth.dynamic_earthnet(synth.SEEDS[4] + idx, shp)
+    else:
+        x = synth.era5(synth.SEEDS[5], shp, t0=idx * shp[0])
+    _SAMPLE["x"] = x.numpy()
+    _SAMPLE["cfg"] = cfg
+
+
+def _cpu_run(_):
+    """The worker's sample through the oracle port: fill -> [normalise -> PCA] ->
+    fit_quant -> quantise -> planar frames -> dequantise -> [inverse] -> PSNR [+ SSIM]."""
     import numpy as np
 
     from oracle import cubevid_oracle as O
     from oracle import metrics_oracle as M
+    from paper_2506_19656_b200 import synth
 
+    x = _SAMPLE["x"]
+    c = synth.CONFIGS[_SAMPLE["cfg"]]
     t0 = time.perf_counter()
-    enc = O.encode_stream(x, 10)
-    rec = O.decode_stream(enc["frames"], enc, x.shape, 10)
+    enc = O.encode_stream(x, c["bit_depth"], n_pcs=c["n_pcs"], normalize=c.get("normalize", False))
+    rec = O.decode_stream(enc["frames"], enc, x.shape, c["bit_depth"])
     M.psnr_per_band(enc["filled"], rec)
-    M.ssim_per_band(enc["filled"], rec)
+    if c["ssim"]:
+        M.ssim_per_band(enc["filled"], rec)
     return int(np.prod(x.shape)), time.perf_counter() - t0
 
 
 class CpuArm:
-    """The reference's algorithm (oracle port of cubevid's numpy functions +
-    the restated metrics) on the host cores: one worker process per core, each
-    processing its own config-2 cube sample (cubes are independent)."""
+    """One worker process per host core, each with its own sample of the workload."""
 
-    def __init__(self, workers: int, t_sample: int):
+    def __init__(self, cfg: int, workers: int):
         import multiprocessing as mp
 
-        from paper_2506_19656_b200 import synth
-
+        self.cfg = cfg
         self.workers = workers
-        self.t_sample = t_sample
-        shape = (t_sample,) + SHAPE2[1:]
-        self.cubes = [synth.minicube(SEED0 + i, shape, device="cpu").numpy() for i in range(workers)]
         ctx = mp.get_context("spawn")
-        self.pool = ctx.Pool(workers) if workers > 1 else None
+        counter = ctx.Value("i", 0)
+        self.pool = ctx.Pool(workers, initializer=_cpu_init, initargs=(cfg, counter))
+        self.pool.map(_noop, range(workers), chunksize=1)  # wait until every sample exists
 
     def step(self) -> tuple:
         t0 = time.perf_counter()
-        if self.pool is None:
-            res = [_cpu_worker(self.cubes[0])]
-        else:
-            res = self.pool.map(_cpu_worker, self.cubes, chunksize=1)
+        res = self.pool.map(_cpu_run, range(self.workers), chunksize=1)
         dt = time.perf_counter() - t0
         return sum(r[0] for r in res), dt
 
     def close(self):
-        if self.pool is not None:
-            self.pool.close()
-            self.pool.join()
+        self.pool.close()
+        self.pool.join()
 
     def sample_text(self) -> str:
-        return (f"{self.workers} worker process(es) x one [{self.t_sample},128,128,7] f32 minicube "
-                f"(config-2 generator, {self.t_sample}/495 time steps) per step, full pipeline "
-                "fill/stats/10-bit quantise/planar/dequantise/PSNR/SSIM-11x11")
+        T, H, W, C = _sample_shape(self.cfg)
+        return (f"{self.workers} worker process(es) x one [{T},{H},{W},{C}] sample of config {self.cfg} "
+                "(same generator) per step through the oracle port of cubevid's numpy functions + the "
+                "restated metrics (full fill/[normalise+PCA]/quantise/planar/dequantise/[inverse]/"
+                "PSNR[/SSIM] pipeline)")
+
+
+def _noop(_):
+    return 0
 
 
 def _cpu_workers():
@@ -279,7 +349,7 @@ def run_reference(a):
     if rank != 0:
         return 0
     workers = _cpu_workers()
-    arm = CpuArm(workers, t_sample=124)
+    arm = CpuArm(a.config, workers)
     for _ in range(a.warmup):
         arm.step()
     tot_e, tot_t = 0, 0.0
@@ -289,12 +359,12 @@ def run_reference(a):
         tot_t += dt
     arm.close()
     value = tot_e / tot_t / 1e9
-    wl = Workload(2, 0, 1, a.cubes)
+    wl = Workload(a.config, 0, a.gpus, a.cubes, a.t)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * tot_t / a.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": wl.config_json(1),
+        "scaling": "weak" if a.config == 2 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": wl.config_json(a.gpus),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": arm.sample_text()},
@@ -320,7 +390,7 @@ def run_ours(a):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    _lib.load()
+    lib = _lib.load()
 
     wl = Workload(a.config, rank, world, a.cubes, a.t)
     x = wl.make_input(dev, rank)
@@ -354,10 +424,10 @@ def run_ours(a):
             ev.append(marks)
         return enc, sc
 
-    for _ in range(a.warmup):
+    for _ in range(max(3, a.warmup)):
         step()
     torch.cuda.synchronize(dev)
-    # numerics sanity of the warm state (outside the timed region)
+    # numerics of the warm state (outside the timed region)
     enc, sc = step()
     enc.check()
     rep0 = sc.report()[0]
@@ -368,6 +438,7 @@ def run_ours(a):
     torch.cuda.synchronize(dev)
     clocks.start()
     time.sleep(0.3)
+    n0 = lib.cv_launch_count()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -375,6 +446,7 @@ def run_ours(a):
         step(record=True)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
+    launches = lib.cv_launch_count() - n0
     ms = t_start.elapsed_time(t_end)
     if world > 1:
         dist.barrier()
@@ -411,10 +483,11 @@ def run_ours(a):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "warmup": max(3, a.warmup), "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if a.config == 2 else "strong",
         "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator with the configuration's statistics, generated on device)",
+        "data": "synthetic (seeded generator with the configuration's shapes and statistics, generated "
+                "on device)",
         "config": wl.config_json(world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"],
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
@@ -423,30 +496,30 @@ def run_ours(a):
                      "pipeline_alg_bytes_per_elem": wl.alg_total,
                      "pipeline_frac": value * 1e9 * wl.alg_total / world / (peak * 1e9)},
         "kernels": kernels,
-        "gpu_launches": None,
+        "gpu_launches": int(launches),
         "clocks": clk,
         "numerics": {"psnr_db_cube0": rep0["psnr"], "ssim_cube0": rep0.get("ssim"), "bpppb": rep0["bpppb"]},
     }
-    # our kernels per step: stats (reset, stats, finalize) + quantize + eval (+finalize); PCA adds
-    # gram (+reduce), stats reset/finalize and projection per cube
-    line["gpu_launches"] = a.steps * (6 if not wl.n_pcs else 9)
 
-    # end-to-end through the public API with pinned host buffers (config 2)
-    if a.config == 2 and not a.no_e2e and not a.profile:
+    # end to end through the public API: pinned host cube -> device -> frames -> host
+    # (codec hand-off) -> decoded frames -> device -> recon + metrics -> host
+    if not a.no_e2e and not a.profile:
         host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
         host.copy_(x)
-        del recon
-        streamer = pipeline.HostStreamer(tuple(x.shape), x.dtype, spec, chunk=8, device=dev)
-        del x
+        shape5 = tuple(x.shape) if x.dim() == 5 else (1,) + tuple(x.shape)
+        del recon, x, wsp, enc, sc
         torch.cuda.empty_cache()
-        streamer.run(host)  # warm-up
+        streamer = pipeline.HostStreamer(shape5, host.dtype, spec, chunk=8 if a.config == 2 else 1,
+                                         want_ssim=wl.ssim, device=dev, shard=shard)
+        host5 = host.view(shape5)
+        streamer.run(host5)  # warm-up
         k_e2e = max(1, min(a.steps, 3))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         for _ in range(k_e2e):
-            streamer.run(host)  # ends with the D2H read of the metric sums (synchronising)
+            streamer.run(host5)  # ends with the D2H read of the metric sums (synchronising)
         torch.cuda.synchronize(dev)
         dt = (time.perf_counter() - t0) / k_e2e
         if world > 1:
@@ -455,11 +528,17 @@ def run_ours(a):
             dt = float(tt.item())
         line["e2e"] = {"value": wl.elem_total / dt / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": streamer.h2d_bytes, "d2h_bytes_per_step": streamer.d2h_bytes,
-                       "ms_per_step": dt * 1e3, "path": "pipeline.HostStreamer (pinned host, 8-cube "
-                       "chunks, copy stream overlapped with the kernels)"}
+                       "ms_per_step": dt * 1e3,
+                       "path": "pipeline.HostStreamer: pinned host cube -> encode_prep -> each [b][g] frame "
+                               "slice D2H into pinned host memory (codec hand-off) -> decoded frames H2D -> "
+                               "decode_eval -> metric sums D2H"
+                               + (" (8-cube chunks, copies overlapped with the kernels)" if a.config == 2
+                                  else "")}
+        del streamer, host, host5
+        torch.cuda.empty_cache()
 
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.profile:
-        arm = CpuArm(_cpu_workers(), t_sample=124)
+        arm = CpuArm(a.config, _cpu_workers())
         e, dt = arm.step()
         arm.close()
         line["cpu_baseline"] = {"value": e / dt / 1e9, "unit": UNIT, "cores": arm.workers, "kind": "port",
@@ -474,6 +553,9 @@ def run_ours(a):
 
 def main():
     a = _args()
+    rc = _maybe_spawn(a)
+    if rc is not None:
+        return rc
     if a.impl == "reference":
         return run_reference(a)
     return run_ours(a)

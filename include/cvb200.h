@@ -66,6 +66,8 @@ const char *cv_status_string(int status);
 const char *cv_last_error(void);
 /* largest channel count the kernels accept (per stream) */
 int cv_max_channels(void);
+/* number of kernels this library has launched in the process (benchmark accounting) */
+unsigned long long cv_launch_count(void);
 
 /* ---------------------------------------------------------------------- */
 /* K1 — per-band statistics (+ forward-fill segment carries)               */
@@ -106,13 +108,22 @@ int cv_stats_finalize(const void *stats_ws, int64_t n_cubes, int32_t C,
                       int32_t fill_mode, float fill_value, double *mins,
                       double *maxs, int64_t *nan_counts, void *stream);
 
+/*
+ * Per (cube, band) leading-gap flag of a fill-mode statistics workspace
+ * (1 = some t=0 cell of the band was NaN, so the leading fill constant enters
+ * the band's range, cube.py:236-242): lead [n_cubes][C] int32. Time-sharded
+ * streams combine the flag of the first shard only (dist.py).
+ */
+int cv_stats_lead_flags(const void *stats_ws, int64_t n_cubes, int32_t C,
+                        int32_t *lead, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* forward_fill_time (cube.py:213-246)                                      */
 /* ---------------------------------------------------------------------- */
 
 /*
  * src/out: [n_outer][T][inner] f32 (time axis moved to position 1 by the
- * caller's strides); mask: same shape, 1 = observed (ValidityMask).
+ * caller's strides); mask (nullable): same shape, 1 = observed (ValidityMask).
  * seg_last: carry map produced by cv_stats(fill_mode=1, seg_len) over the
  * same geometry (C = 1 is fine). carry_in (nullable, [n_outer][inner], NaN =
  * none): values carried in from earlier time shards (multi-GPU T-sharding).

@@ -36,11 +36,13 @@ SIGNATURES = {
     "cv_status_string": ([_INT], ctypes.c_char_p),
     "cv_last_error": ([], ctypes.c_char_p),
     "cv_max_channels": ([], _INT),
+    "cv_launch_count": ([], ctypes.c_ulonglong),
     "cv_stats_ws_bytes": ([_I64, _I32], _SZ),
     "cv_num_segments": ([_I64, _I32], _I64),
     "cv_stats_reset": ([_P, _I64, _I32, _P], _INT),
     "cv_stats": ([_P, _I32, _I64, _I64, _I64, _I32, _I32, _I32, _P, _P, _P, _P], _INT),
     "cv_stats_finalize": ([_P, _I64, _I32, _I32, _F32, _P, _P, _P, _P], _INT),
+    "cv_stats_lead_flags": ([_P, _I64, _I32, _P, _P], _INT),
     "cv_forward_fill": ([_P, _I64, _I64, _I64, _F32, _I32, _P, _P, _P, _P, _P, _P], _INT),
     "cv_quantize": ([_P, _I32, _I64, _I64, _I64, _I32, _P, _P, _I32, _I32, _I32, _F32, _I32, _P,
                      _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P], _INT),

@@ -1,11 +1,15 @@
 // Host-side glue of the C ABI: status strings, last-error, launch checks.
 #include <stdarg.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace cvb {
 
 static thread_local std::string g_last_error;
+// kernels launched through this library (every launch site calls check_launch once)
+static std::atomic<unsigned long long> g_launches{0};
 
 void set_last_error(const std::string &msg) { g_last_error = msg; }
 
@@ -20,6 +24,7 @@ int fail(int status, const char *fmt, ...) {
 }
 
 int check_launch(const char *what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(CV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return CV_OK;
@@ -45,5 +50,7 @@ const char *cv_status_string(int status) {
 const char *cv_last_error(void) { return cvb::g_last_error.c_str(); }
 
 int cv_max_channels(void) { return cvb::kMaxC; }
+
+unsigned long long cv_launch_count(void) { return cvb::g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

@@ -231,6 +231,11 @@ k_stats_vec(const TIn *__restrict__ src, int64_t T, int64_t inner, int C, int fi
   }
 }
 
+__global__ void k_stats_lead(const StatsEntry *__restrict__ ws, int64_t n, int32_t *__restrict__ lead) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) lead[i] = ws[i].lead ? 1 : 0;
+}
+
 __global__ void k_stats_finalize(const StatsEntry *__restrict__ ws, int64_t n, int fill_mode,
                                  float fill, double *mins, double *maxs, int64_t *nan_counts) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -286,7 +291,7 @@ k_forward_fill(const float *__restrict__ src, int64_t T, int64_t inner, float fi
         carry[k] = v;
       }
       out[off + e] = carry[k];
-      mask[off + e] = ok ? 1 : 0;
+      if (mask) mask[off + e] = ok ? 1 : 0;
     }
   }
   flag_warp(err, inf_seen, CV_FLAG_NONFINITE);
@@ -377,10 +382,19 @@ int cv_stats_finalize(const void *stats_ws, int64_t n_cubes, int32_t C, int32_t 
   return check_launch("cv_stats_finalize");
 }
 
+int cv_stats_lead_flags(const void *stats_ws, int64_t n_cubes, int32_t C, int32_t *lead, void *stream) {
+  if (!stats_ws || !lead || C <= 0 || n_cubes < 0) return fail(CV_ERR_ARG, "cv_stats_lead_flags: bad arguments");
+  const int64_t n = n_cubes * C;
+  if (n == 0) return CV_OK;
+  k_stats_lead<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>((const StatsEntry *)stats_ws, n,
+                                                                              lead);
+  return check_launch("cv_stats_lead_flags");
+}
+
 int cv_forward_fill(const float *src, int64_t n_outer, int64_t T, int64_t inner, float fill_value,
                     int32_t seg_len, const float *seg_last, const float *carry_in, float *out,
                     uint8_t *mask, uint32_t *err_word, void *stream) {
-  if (!src || !out || !mask || !seg_last) return fail(CV_ERR_ARG, "cv_forward_fill: null pointer");
+  if (!src || !out || !seg_last) return fail(CV_ERR_ARG, "cv_forward_fill: null pointer");
   if (n_outer < 0 || T < 0 || inner < 0 || seg_len <= 0) return fail(CV_ERR_SHAPE, "cv_forward_fill: bad sizes");
   if (n_outer > 65535 || cv_num_segments(T, seg_len) > 65535)
     return fail(CV_ERR_UNSUPPORTED, "cv_forward_fill: grid too large");

@@ -115,6 +115,16 @@ class TimeShard:
             N += n_r
         return s0, np.concatenate([S, G.reshape(-1)]), int(round(N))
 
+    def combine_flags(self, flags: int) -> int:
+        """OR of every rank's device error flags (CV_FLAG_*), so that all ranks
+        take the same branch (fill first, or raise together) instead of one rank
+        raising while the others wait in a later collective."""
+        bits = torch.tensor([(flags >> i) & 1 for i in range(8)], dtype=torch.int64)
+        if not self.host_staging:
+            bits = bits.to(torch.device("cuda", torch.cuda.current_device()))
+        self.all_reduce(bits, dist.ReduceOp.MAX)
+        return int(sum(int(b) << i for i, b in enumerate(bits.cpu().tolist())))
+
     def combine_scores(self, sse: torch.Tensor, ssim_sum: torch.Tensor):
         t = torch.cat([sse.reshape(-1), ssim_sum.reshape(-1)]).to(torch.float64)
         self.all_reduce(t)
@@ -148,5 +158,6 @@ def raw_band_stats(x: dev.Arr, B: int, T: int, inner: int, C: int, fill_mode: in
     nans = torch.empty((B, C), dtype=torch.int64, device=d)
     _lib.call("cv_stats_finalize", ws.data_ptr(), B, C, 0, 0.0, mins.data_ptr(), maxs.data_ptr(),
               nans.data_ptr(), s)
-    lead = ws[: B * C * 32].view(torch.int32).view(B, C, 8)[..., 6].clone()
+    lead = torch.empty((B, C), dtype=torch.int32, device=d)
+    _lib.call("cv_stats_lead_flags", ws.data_ptr(), B, C, lead.data_ptr(), s)
     return mins, maxs, lead, nans

@@ -164,46 +164,87 @@ def _fold(model: PcaModel, offset=None, scale=None) -> PcaFold:
                    np.ascontiguousarray(fwd_mean), np.ascontiguousarray(inv), offset, scale)
 
 
-def fit_pca(x: dev.Arr, cube: int, T: int, HW: int, C: int, n_pcs: int, normalize: bool,
-            shard=None):
-    """K2 pass (Gram + band stats) -> host eigh -> folded model; returns (fold, mins, maxs).
+def _cube_view(x: dev.Arr, b: int, T: int, HW: int, C: int) -> dev.Arr:
+    return dev.Arr(x.t[b] if x.t.dim() == 5 else x.t, x.code, x.host, x.np_dtype, (T, HW, C))
 
-    With a multi-rank ``shard`` the Gram partials and band ranges of all time
-    shards are combined first, so every rank fits the same model.
+
+def _launch_grams(x: dev.Arr, B: int, T: int, HW: int, C: int, err: dev.ErrWord) -> list:
+    """K2 (float64 shifted Gram + band min/max) of every cube; device-side only."""
+    return [gram(_cube_view(x, b, T, HW, C), T * HW, C, stats=True, err=err) for b in range(B)]
+
+
+def _fit_models(grams: list, n: int, C: int, n_pcs: int, normalize: bool, shard=None):
+    """Gram partials -> host eigh -> folded models; one device->host copy for all cubes.
+
+    With a multi-rank ``shard`` every rank re-centres the gathered partials on
+    rank 0's shift, so all ranks fit the identical model.
     """
-    n = T * HW
-    view = dev.Arr(x.t[cube] if x.t.dim() == 5 else x.t, x.code, x.host, x.np_dtype, (T, HW, C))
-    g = gram(view, n, C, stats=True)
-    if g["err"].flags() & (_lib.CV_FLAG_NAN | _lib.CV_FLAG_NONFINITE):
-        raise ConfigurationError("cannot fit a PCA on non-finite values")
-    if shard is not None and shard.world > 1:
-        shift, out, n = shard.combine_gram(g["shift"], g["out"], n, C)
-        gmins, gmaxs = shard.combine_minmax(g["mins"], g["maxs"])
-        g["mins"], g["maxs"] = gmins, gmaxs
-    else:
-        out = g["out"].cpu().numpy()
-        shift = g["shift"].double().cpu().numpy()
-    mins = g["mins"].cpu().numpy()
-    maxs = g["maxs"].cpu().numpy()
-    mean, cov = covariance_from_gram(shift, out, n, C)
-    if normalize:
-        scale = maxs - mins
-        scale = np.where(scale == 0, 1.0, scale)
-        zmean = (mean - mins) / scale
-        zcov = cov / np.outer(scale, scale)
-        model = eig_model(zmean, zcov, n_pcs, C)
-        return _fold(model, mins, scale), g["mins"], g["maxs"]
-    return _fold(eig_model(mean, cov, n_pcs, C)), g["mins"], g["maxs"]
+    sharded = shard is not None and shard.world > 1
+    folds, peaks = [], []
+    if not sharded:
+        pack = torch.stack([torch.cat([g["shift"].double(), g["out"], g["mins"], g["maxs"]])
+                            for g in grams]).cpu().numpy()
+    for b, g in enumerate(grams):
+        if sharded:
+            shift, out, nn = shard.combine_gram(g["shift"], g["out"], n, C)
+            gmins, gmaxs = shard.combine_minmax(g["mins"], g["maxs"])
+            mins, maxs = gmins.cpu().numpy(), gmaxs.cpu().numpy()
+            peaks.append(gmaxs)
+        else:
+            row = pack[b]
+            shift, out = row[:C], row[C:2 * C + C * C]
+            mins, maxs = row[2 * C + C * C:3 * C + C * C], row[3 * C + C * C:]
+            nn = n
+            peaks.append(g["maxs"])
+        mean, cov = covariance_from_gram(shift, out, nn, C)
+        if normalize:
+            scale = maxs - mins
+            scale = np.where(scale == 0, 1.0, scale)
+            zmean = (mean - mins) / scale
+            zcov = cov / np.outer(scale, scale)
+            folds.append(_fold(eig_model(zmean, zcov, n_pcs, C), mins, scale))
+        else:
+            folds.append(_fold(eig_model(mean, cov, n_pcs, C)))
+    return folds, torch.stack(peaks)
+
+
+def _fill_stats(x: dev.Arr, spec: StreamSpec, B: int, T: int, HW: int, C: int, err: dev.ErrWord,
+                workspace, shard):
+    """K1 in fill mode (forward-fill carries + per-band ranges of the filled cube).
+
+    Returns (qmins, qmaxs, nan_counts, seg_last, carry_in); in a time-sharded
+    stream the ranges are global and ``carry_in`` holds the last observation
+    of the earlier shards.
+    """
+    lib = _lib.load()
+    d = x.device
+    nseg = lib.cv_num_segments(T, spec.seg_len)
+    seg_last = _alloc(workspace, "seg_last", (B, nseg, HW * C), torch.float32, d)
+    if shard is None or shard.world == 1:
+        qmins, qmaxs, nans = band_stats(x, B, T, HW * C, C, fill_mode=1, seg_len=spec.seg_len,
+                                        fill_value=spec.fill_value, err=err, seg_last=seg_last)
+        return qmins, qmaxs, nans, seg_last, None
+    from .dist import last_observed, raw_band_stats
+
+    mins, maxs, lead, nans = raw_band_stats(x, B, T, HW * C, C, 1, spec.seg_len, err, seg_last)
+    qmins, qmaxs, nans = shard.combine_band_stats(mins, maxs, lead, nans, spec.fill_value)
+    return qmins, qmaxs, nans, seg_last, shard.carry_in(last_observed(seg_last))
 
 
 def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | None = None,
                 shard=None, workspace: Workspace | None = None) -> Encoded:
-    """Cube(s) -> planar integer frames + QuantParams (+ PCA models).
+    """Cube(s) -> planar integer frames + QuantParams (+ PCA models), SPEC.md:351.
 
-    Float32 cubes are forward-filled on the fly; the quantiser also writes the
-    filled cube (``Encoded.filled``, forward_fill_time's output) so decode can
-    score against what the codec saw. ``marks`` (optional callable) is invoked
-    with a phase label after the statistics phase (benchmark CUDA events).
+    Float32 cubes are forward-filled (cube.py:213-246) before anything else
+    sees them. Without PCA the fill is fused into the quantiser, which also
+    writes the filled cube (``Encoded.filled``, forward_fill_time's output) so
+    decode scores against what the codec saw. With PCA the Gram pass runs on
+    the raw cube first; if it met NaN (every rank agrees through one
+    all-reduce of the error flags) the cube is forward-filled into the
+    workspace and the Gram, projection and quantiser read the filled copy,
+    as the reference's pca_fit is fed the filled array (transform.py:160-188).
+    ``marks`` (optional callable) is invoked with a phase label after the
+    statistics phase (benchmark CUDA events).
     """
     x, (B, T, H, W, C) = _as_batch(cube)
     d = x.device
@@ -217,71 +258,86 @@ def encode_prep(cube, spec: StreamSpec, marks=None, filled_out: torch.Tensor | N
     lib = _lib.load()
     sharded = shard is not None and shard.world > 1
     carry_in = None
+    filled = None
     if spec.n_pcs == 0:
         E = C
         seg_last = None
         if fill:
-            nseg = lib.cv_num_segments(T, seg)
-            seg_last = _alloc(workspace, "seg_last", (B, nseg, HW * C), torch.float32, d)
-        if not sharded:
-            qmins, qmaxs, nans = band_stats(x, B, T, HW * C, C, fill_mode=int(fill), seg_len=seg,
-                                            fill_value=spec.fill_value, err=err, seg_last=seg_last)
+            qmins, qmaxs, nans, seg_last, carry_in = _fill_stats(x, spec, B, T, HW, C, err, workspace,
+                                                                 shard)
+        elif not sharded:
+            qmins, qmaxs, nans = band_stats(x, B, T, HW * C, C, fill_mode=0, seg_len=seg, err=err)
         else:
-            from .dist import last_observed, raw_band_stats
+            from .dist import raw_band_stats
 
-            mins, maxs, lead, nans = raw_band_stats(x, B, T, HW * C, C, int(fill), seg, err, seg_last)
+            mins, maxs, lead, nans = raw_band_stats(x, B, T, HW * C, C, 0, seg, err, None)
             qmins, qmaxs, nans = shard.combine_band_stats(mins, maxs, lead, nans, spec.fill_value)
-            if fill:
-                carry_in = shard.carry_in(last_observed(seg_last))
         peaks = qmaxs
         folds = []
+        src = x
     else:
         if spec.n_pcs > C:
             raise ConfigurationError(f"n_keep={spec.n_pcs} outside [1, {C}]")
         E = spec.n_pcs
         seg_last, nans = None, None
-        folds = []
+        src = x
+        gerr = dev.ErrWord(d)
+        grams = _launch_grams(src, B, T, HW, C, gerr)
+        flags = gerr.flags()
+        if sharded:
+            flags = shard.combine_flags(flags)
+        if flags & _lib.CV_FLAG_NONFINITE:
+            raise ConfigurationError("array contains +/-inf; only NaN marks missing data")
+        if flags & _lib.CV_FLAG_NAN:
+            if not fill:
+                raise ConfigurationError("cannot fit a PCA on non-finite values")
+            # fill (+mask) before pca_fit / pca_forward
+            _, _, nans, seg_last, carry_in = _fill_stats(x, spec, B, T, HW, C, err, workspace, shard)
+            filled = filled_out if filled_out is not None else _alloc(workspace, "filled", x.t.shape,
+                                                                      x.t.dtype, d)
+            _lib.call("cv_forward_fill", x.ptr, B, T, HW * C, float(spec.fill_value), seg,
+                      seg_last.data_ptr(), carry_in.data_ptr() if carry_in is not None else None,
+                      filled.data_ptr(), None, err.ptr, s)
+            src = dev.Arr(filled, x.code, x.host, x.np_dtype, x.shape)
+            gerr.reset()
+            grams = _launch_grams(src, B, T, HW, C, gerr)
+        folds, peaks = _fit_models(grams, T * HW, C, E, spec.normalize, shard)
         qmins = torch.empty((B, E), dtype=torch.float64, device=d)
         qmaxs = torch.empty_like(qmins)
-        peaks = torch.empty((B, C), dtype=torch.float64, device=d)
+        sws = dev.workspace(lib.cv_stats_ws_bytes(B, E), d)
+        _lib.call("cv_stats_reset", sws.data_ptr(), B, E, s)
+        esz = lib.cv_stats_ws_bytes(1, E)
         for b in range(B):
-            fold, bmins, bmaxs = fit_pca(x, b, T, HW, C, E, spec.normalize, shard)
-            folds.append(fold)
-            peaks[b] = bmaxs
-            sws = dev.workspace(lib.cv_stats_ws_bytes(1, E), d)
-            _lib.call("cv_stats_reset", sws.data_ptr(), 1, E, s)
-            src_b = x.t[b] if x.t.dim() == 5 else x.t
-            _lib.call("cv_pca_project", src_b.data_ptr(), x.code, 1, T * HW, C,
+            fold = folds[b]
+            _lib.call("cv_pca_project", _cube_view(src, b, T, HW, C).ptr, src.code, 1, T * HW, C,
                       fold.fwd_mean.ctypes.data, fold.fwd_comps.ctypes.data, E, None, _lib.CV_F64,
-                      sws.data_ptr(), err.ptr, s)
-            _lib.call("cv_stats_finalize", sws.data_ptr(), 1, E, 0, 0.0, qmins[b:].data_ptr(),
-                      qmaxs[b:].data_ptr(), None, s)
-            if sharded:
-                qmins[b], qmaxs[b] = shard.combine_minmax(qmins[b], qmaxs[b])
+                      sws.data_ptr() + b * esz, err.ptr, s)
+        _lib.call("cv_stats_finalize", sws.data_ptr(), B, E, 0, 0.0, qmins.data_ptr(),
+                  qmaxs.data_ptr(), None, s)
+        if sharded:
+            qmins, qmaxs = shard.combine_minmax(qmins, qmaxs)
     if marks is not None:
         marks("stats")
     groups = pack_groups(E)
     G = len(groups)
     tdt, _ = dev.out_dtype_for_depth(spec.bit_depth)
     frames = _alloc(workspace, "frames", (B, G, T, 3, HW), tdt, d)
-    filled = None
-    if spec.n_pcs == 0 and fill:
-        filled = filled_out if filled_out is not None else _alloc(workspace, "filled", x.t.shape,
-                                                                  x.t.dtype, d)
-    for b in range(B) if spec.n_pcs else [None]:
-        if b is None:
-            _lib.call("cv_quantize", x.ptr, x.code, B, T, HW, C, qmins.data_ptr(), qmaxs.data_ptr(),
-                      spec.bit_depth, int(spec.clamp), int(fill), float(spec.fill_value), seg,
-                      seg_last.data_ptr() if seg_last is not None else None,
-                      carry_in.data_ptr() if carry_in is not None else None, None, None, 0,
-                      _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames.data_ptr(),
-                      filled.data_ptr() if filled is not None else None, err.ptr, s)
-        else:
+    if spec.n_pcs == 0:
+        if fill:
+            filled = filled_out if filled_out is not None else _alloc(workspace, "filled", x.t.shape,
+                                                                      x.t.dtype, d)
+        _lib.call("cv_quantize", x.ptr, x.code, B, T, HW, C, qmins.data_ptr(), qmaxs.data_ptr(),
+                  spec.bit_depth, int(spec.clamp), int(fill), float(spec.fill_value), seg,
+                  seg_last.data_ptr() if seg_last is not None else None,
+                  carry_in.data_ptr() if carry_in is not None else None, None, None, 0,
+                  _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames.data_ptr(),
+                  filled.data_ptr() if filled is not None else None, err.ptr, s)
+    else:
+        for b in range(B):
             fold = folds[b]
-            src_b = x.t[b] if x.t.dim() == 5 else x.t
-            _lib.call("cv_quantize", src_b.data_ptr(), x.code, 1, T, HW, C, qmins[b:].data_ptr(),
-                      qmaxs[b:].data_ptr(), spec.bit_depth, int(spec.clamp), 0, 0.0, seg, None, None,
-                      fold.fwd_mean.ctypes.data, fold.fwd_comps.ctypes.data, E,
+            _lib.call("cv_quantize", _cube_view(src, b, T, HW, C).ptr, src.code, 1, T, HW, C,
+                      qmins[b:].data_ptr(), qmaxs[b:].data_ptr(), spec.bit_depth, int(spec.clamp), 0,
+                      0.0, seg, None, None, fold.fwd_mean.ctypes.data, fold.fwd_comps.ctypes.data, E,
                       _lib.CV_LAYOUT_PLANAR, _PAD[spec.pad_mode], frames[b].data_ptr(), None,
                       err.ptr, s)
     enc = Encoded(frames, qmins, qmaxs, spec, (B, T, H, W, C), groups, peaks, nans, seg_last,
@@ -394,29 +450,50 @@ def roundtrip(cube, spec: StreamSpec, want_ssim: bool = True, want_recon: bool =
 
 
 class HostStreamer:
-    """Round trips of host-resident cube batches with the host->device copies
-    overlapped with the kernels: chunks of cubes are copied from pinned host
-    memory on a copy stream into a double buffer while the previous chunk is
-    encoded, decoded and scored on the compute stream. Only the per-band metric
-    sums come back to the host.
+    """End-to-end round trips of host-resident cubes through the public API,
+    including the codec hand-off on both sides (SPEC.md:351/360,
+    bridge.py:157-160, 213-230, 288-303).
+
+    Per chunk of cubes: the cube is copied from pinned host memory (H2D copy
+    stream) -> ``encode_prep`` -> every ``[b][g]`` frame slice (the bytes
+    ``_frames_to_planar_bytes`` hands ffmpeg for video g) is copied into
+    pinned host frames, one ``cudaMemcpyAsync`` per slice (D2H copy stream)
+    -> the codec's decoded frames are copied back (H2D; the benchmark's codec
+    is the identity, so they are the same bytes) -> ``decode_eval`` scores them
+    -> the per-band metric sums come back to the host. With more than one
+    chunk the copies of one chunk overlap the kernels of the other (two
+    buffer sets). ``shard`` (dist.TimeShard) runs a time-sharded stream.
     """
 
     def __init__(self, shape, dtype, spec: StreamSpec, chunk: int, want_ssim: bool = True,
-                 device=None):
+                 device=None, handoff: bool = True, shard=None):
         self.B, self.T, self.H, self.W, self.C = shape
         self.spec = spec
         self.chunk = max(1, min(chunk, self.B))
         self.want_ssim = want_ssim
+        self.handoff = handoff
+        self.shard = shard
         self.device = device or dev.default_device()
+        nchunks = (self.B + self.chunk - 1) // self.chunk
+        self.nbuf = 2 if nchunks > 1 else 1
         per = (self.chunk, self.T, self.H, self.W, self.C)
-        self.bufs = [torch.empty(per, dtype=dtype, device=self.device) for _ in range(2)]
+        self.bufs = [torch.empty(per, dtype=dtype, device=self.device) for _ in range(self.nbuf)]
         self.recon = torch.empty(per, dtype=torch.float32, device=self.device)
-        self.copy_stream = torch.cuda.Stream(self.device)
-        self.ready = [torch.cuda.Event() for _ in range(2)]
-        self.free = [torch.cuda.Event() for _ in range(2)]
+        self.h2d_stream = torch.cuda.Stream(self.device)
+        self.d2h_stream = torch.cuda.Stream(self.device)
+        self.ready = [torch.cuda.Event() for _ in range(self.nbuf)]
+        self.free = [torch.cuda.Event() for _ in range(self.nbuf)]
+        self.ws = [Workspace() for _ in range(self.nbuf)]
+        E = spec.n_pcs or self.C
+        G = (E + 2) // 3
+        tdt, _ = dev.out_dtype_for_depth(spec.bit_depth)
+        fshape = (self.chunk, G, self.T, 3, self.H * self.W)
+        self.host_frames = None
+        if handoff:
+            self.host_frames = [torch.empty(fshape, dtype=tdt, pin_memory=True) for _ in range(self.nbuf)]
+            self.dec = [torch.empty(fshape, dtype=tdt, device=self.device) for _ in range(self.nbuf)]
         self.h2d_bytes = 0
         self.d2h_bytes = 0
-        self.ws = [Workspace(), Workspace()]
 
     def run(self, host: torch.Tensor) -> list:
         """host: pinned [B,T,H,W,C]; returns one metric report per cube."""
@@ -424,39 +501,70 @@ class HostStreamer:
         sse, ssim, peaks = [], [], []
         starts = list(range(0, self.B, self.chunk))
         self.h2d_bytes = 0
+        self.d2h_bytes = 0
 
         def issue(i):
-            k = i % 2
+            k = i % self.nbuf
             s0 = starts[i]
             n = min(self.chunk, self.B - s0)
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(self.free[k])
+            with torch.cuda.stream(self.h2d_stream):
+                self.h2d_stream.wait_event(self.free[k])
                 self.bufs[k][:n].copy_(host[s0:s0 + n], non_blocking=True)
-                self.ready[k].record(self.copy_stream)
+                self.ready[k].record(self.h2d_stream)
             self.h2d_bytes += host[s0:s0 + n].numel() * host.element_size()
 
-        for k in range(2):
+        for k in range(self.nbuf):
             self.free[k].record(comp)
         issue(0)
         scores = None
         for i, s0 in enumerate(starts):
-            k = i % 2
+            k = i % self.nbuf
             n = min(self.chunk, self.B - s0)
-            if i + 1 < len(starts):
+            if i + 1 < len(starts) and self.nbuf > 1:
                 issue(i + 1)
             comp.wait_event(self.ready[k])
             x = self.bufs[k][:n]
-            enc = encode_prep(x, self.spec, workspace=self.ws[k])
-            _, scores = decode_eval(enc, x, want_ssim=self.want_ssim, recon_out=self.recon[:n])
+            enc = encode_prep(x, self.spec, workspace=self.ws[k], shard=self.shard)
+            frames = None
+            if self.handoff:
+                frames = self._handoff(enc, k, n, comp)
+            _, scores = decode_eval(enc, x, frames=frames, want_ssim=self.want_ssim,
+                                    recon_out=self.recon[:n])
             self.free[k].record(comp)
+            if i + 1 < len(starts) and self.nbuf == 1:
+                issue(i + 1)
             sse.append(scores.sse)
             ssim.append(scores.ssim_sum)
             peaks.append(scores.peaks)
         allsse = torch.cat(sse).cpu()
         allssim = torch.cat(ssim).cpu()
         allpeaks = torch.cat(peaks).cpu()
-        self.d2h_bytes = 3 * allsse.numel() * 8
+        self.d2h_bytes += 3 * allsse.numel() * 8
         out = Scores(allsse, allssim, allpeaks, scores.n_per_band, scores.n_ssim_per_band,
-                     self.want_ssim, scores.frame_bytes_per_cube,
-                     (self.B, self.T, self.H, self.W, self.C))
+                     self.want_ssim, scores.frame_bytes_per_cube, (self.B,) + tuple(scores.shape[1:]))
         return out.report()
+
+    def _handoff(self, enc: Encoded, k: int, n: int, comp) -> torch.Tensor:
+        """Frames -> pinned host (one copy per [b][g] video slice) -> decoded frames -> device."""
+        hf = self.host_frames[k][:n]
+        dec = self.dec[k][:n]
+        done = torch.cuda.Event()
+        done.record(comp)
+        with torch.cuda.stream(self.d2h_stream):
+            self.d2h_stream.wait_event(done)
+            for b in range(n):
+                for g in range(enc.frames.shape[1]):
+                    hf[b, g].copy_(enc.frames[b, g], non_blocking=True)
+            back = torch.cuda.Event()
+            back.record(self.d2h_stream)
+        nbytes = hf.numel() * hf.element_size()
+        self.d2h_bytes += nbytes
+        # the codec runs here on the host bytes; its decoded frames come back
+        with torch.cuda.stream(self.h2d_stream):
+            self.h2d_stream.wait_event(back)
+            dec.copy_(hf, non_blocking=True)
+            arrived = torch.cuda.Event()
+            arrived.record(self.h2d_stream)
+        self.h2d_bytes += nbytes
+        comp.wait_event(arrived)
+        return dec

@@ -194,14 +194,18 @@ def dequantize(q, params: QuantParams):
 
 # ----------------------------------------------------------------------------- PCA
 
-def gram(x: dev.Arr, n_pix: int, C: int, stats: bool = False):
-    """K2: float64 (shift, sums, shifted Gram[, mins, maxs]) of [n_pix][C] spectra."""
+def gram(x: dev.Arr, n_pix: int, C: int, stats: bool = False, err: dev.ErrWord | None = None):
+    """K2: float64 (shift, sums, shifted Gram[, mins, maxs]) of [n_pix][C] spectra.
+
+    Launch only: every result stays on the device (no host synchronisation).
+    """
     d = x.device
     lib = _lib.load()
     s = dev.stream_ptr(d)
     ws = dev.workspace(lib.cv_gram_ws_bytes(n_pix, C), d)
     out = torch.empty(C + C * C, dtype=torch.float64, device=d)
-    err = dev.ErrWord(d)
+    if err is None:
+        err = dev.ErrWord(d)
     sws = None
     if stats:
         sws = dev.workspace(lib.cv_stats_ws_bytes(1, C), d)

@@ -285,6 +285,43 @@ def test_stream_edge_shapes(cuda, shape, C_pcs, B):
     np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
 
 
+@pytest.mark.parametrize("normalize,bits,n_pcs", [(False, 12, 4), (True, 16, 4), (False, 10, 7)])
+def test_stream_nan_then_pca(cuda, normalize, bits, n_pcs):
+    """a cloudy cube is forward-filled before pca_fit / pca_forward
+    (config-1 generator: 20 % NaN frames + 2 % NaN pixels, leading gaps)."""
+    from paper_2506_19656_b200 import synth
+
+    x = synth.minicube(19656, (20, 24, 36, 7)).numpy()
+    assert np.isnan(x).any()
+    enc, recon, sc = G_pipe.roundtrip(torch.from_numpy(x).to(cuda),
+                                      G_pipe.StreamSpec(bits, n_pcs=n_pcs, normalize=normalize))
+    enc.check()
+    ref = O.encode_stream(x, bits, n_pcs=n_pcs, normalize=normalize)
+    # the filled cube the PCA saw is forward_fill_time's output, bit for bit
+    np.testing.assert_array_equal(enc.filled.cpu().numpy().view(np.uint32),
+                                  ref["filled"].view(np.uint32))
+    assert int(enc.nan_counts.sum()) == int(np.isnan(x).sum())
+    mean_o, comps_o, ev_o = ref["pca"]
+    m = enc.pca[0].model
+    cos = np.abs(np.sum(m.components * comps_o, axis=1))
+    assert (cos >= 1 - 1e-9).all(), cos
+    got = enc.frames[0].cpu().numpy().astype(np.int64)
+    diff = np.abs(got - ref["frames"].astype(np.int64))
+    assert diff.max() <= 1 and (diff > 0).mean() <= 0.02
+    rec_o = O.decode_stream(ref["frames"], ref, x.shape, bits)
+    rep = sc.report()[0]
+    np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o),
+                               atol=PSNR_TOL_DB)
+    np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
+
+
+def test_pca_inf_raises(cuda):
+    x = np.random.default_rng(4).random((3, 12, 12, 5)).astype(np.float32)
+    x[1, 2, 3, 4] = np.inf
+    with pytest.raises(ConfigurationError, match="inf"):
+        G_pipe.encode_prep(torch.from_numpy(x).to(cuda), G_pipe.StreamSpec(12, n_pcs=3))
+
+
 def test_all_nan_and_constant_bands(cuda):
     x = np.random.default_rng(1).random((8, 12, 12, 3)).astype(np.float32)
     x[..., 1] = np.nan          # never observed -> fill constant everywhere -> constant band

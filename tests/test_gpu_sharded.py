@@ -26,6 +26,8 @@ def _make(kind):
 
     if kind == "nan":
         return synth.minicube(123, (30, 24, 40, 7)), dict(bit_depth=10, seg_len=4)
+    if kind == "nan_pca":
+        return synth.minicube(321, (30, 24, 40, 7)), dict(bit_depth=12, n_pcs=4, seg_len=4)
     return synth.simple_s2(shape=(6, 32, 48, 12)), dict(bit_depth=12, n_pcs=5)
 
 
@@ -57,7 +59,7 @@ def _worker(rank, world, port, kind, q):
             dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["nan", "pca"])
+@pytest.mark.parametrize("kind", ["nan", "pca", "nan_pca"])
 def test_two_time_shards_match_single_gpu(cuda, kind):
     from paper_2506_19656_b200 import pipeline as P
 
