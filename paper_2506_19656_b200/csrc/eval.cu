@@ -24,8 +24,7 @@
 
 #include "eval_kernel.cuh"
 #include "ssim_kernel.cuh"
-#include "ssim4_kernel.cuh"
-#include "ssim6_kernel.cuh"
+#include "ssim7_kernel.cuh"
 #include "psnr_kernel.cuh"
 
 #include <cstdlib>
@@ -72,47 +71,27 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
     const int wpc = a.C < kSsimWarpsPerCta ? a.C : kSsimWarpsPerCta;
     dim3 grid((unsigned)(a.nstrips * ncg), (unsigned)a.T, (unsigned)n);
     if constexpr ((RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) && std::is_same<TO, float>::value) {
-      if (a.ssim6) {
-        const int ncg6 = (a.C + k6Chans - 1) / k6Chans;
-        dim3 g6((unsigned)(ssim6_groups(a.W) * ncg6), (unsigned)a.T, (unsigned)n);
-        if (pca) {
-          if constexpr (RS == RS_FRAMES_U16) {
-            const size_t sm = sizeof(Ssim6SharedT<true>);
-#define CV_S6P(EP)                                                                                     \
-  do {                                                                                                 \
-    cudaFuncSetAttribute(k_eval_ssim6<RS, false, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_eval_ssim6<RS, false, EP><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);                             \
+      if (a.ssim7) {
+        constexpr int fsz = RS == RS_FRAMES_U8 ? 1 : 2;
+        const int ngrp = (a.C + k7GB - 1) / k7GB;
+        dim3 g7((unsigned)(ssim7_strips(a.W) * ngrp), (unsigned)a.T, (unsigned)n);
+#define CV_S7(MODE, EP)                                                                                  \
+  do {                                                                                                   \
+    const size_t sm = (size_t)ssim7_geom(a.C, MODE == K7_PCA ? a.E : k7GB, fsz, MODE == K7_LUT).total;    \
+    cudaFuncSetAttribute(k_eval_ssim7<RS, MODE, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_eval_ssim7<RS, MODE, EP><<<g7, k7Threads, sm, st>>>(a, inv);                                       \
   } while (0)
-            if (a.E == 6) CV_S6P(6);
-            else if (a.E == 9) CV_S6P(9);
-            else CV_S6P(k6PcaMax);
-#undef CV_S6P
-          }
+        if (pca) {
+          if (a.E == 6) CV_S7(K7_PCA, 6);
+          else if (a.E == 9) CV_S7(K7_PCA, 9);
+          else CV_S7(K7_PCA, k7PcaMax);
+        } else if (a.bit_depth <= 10) {
+          CV_S7(K7_LUT, 0);
         } else {
-          const size_t sm = sizeof(Ssim6Shared);
-          if (a.bit_depth <= 10) {
-            cudaFuncSetAttribute(k_eval_ssim6<RS, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_eval_ssim6<RS, true, 0><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
-          } else {
-            cudaFuncSetAttribute(k_eval_ssim6<RS, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_eval_ssim6<RS, false, 0><<<g6, 32 * 4 * k6Chans, sm, st>>>(a, inv);
-          }
+          CV_S7(K7_F64, 0);
         }
-        return check_launch("cv_eval(ssim6)");
-      }
-      if (!pca && a.W % 4 == 0 && !getenv("CVB_SSIM_V4")) {
-        const int ncg4 = (a.C + kS4Chans - 1) / kS4Chans;
-        const int ngrp = (int)((a.W + kS4Strips * kSsimStrip - 1) / (kS4Strips * kSsimStrip));
-        dim3 g4((unsigned)(ngrp * ncg4), (unsigned)a.T, (unsigned)n);
-        const size_t sm = sizeof(Ssim4Shared);
-        if (a.bit_depth <= 10) {
-          cudaFuncSetAttribute(k_eval_ssim4<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          k_eval_ssim4<RS, true><<<g4, 32 * kS4Strips * kS4Chans, sm, st>>>(a);
-        } else {
-          cudaFuncSetAttribute(k_eval_ssim4<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-          k_eval_ssim4<RS, false><<<g4, 32 * kS4Strips * kS4Chans, sm, st>>>(a);
-        }
-        return check_launch("cv_eval(ssim4)");
+#undef CV_S7
+        return check_launch("cv_eval(ssim7)");
       }
     }
     if constexpr (RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) {
@@ -182,7 +161,7 @@ size_t cv_eval_ws_bytes(int64_t n_cubes, int64_t T, int64_t H, int64_t W, int32_
   if (C <= 0) return 0;
   const int TX = eval_tx(C, want_ssim != 0);
   int64_t nstrips = (W + TX - 1) / TX;
-  if (want_ssim && W >= kSsimTaps && 4 * (int64_t)ssim6_groups(W) > nstrips) nstrips = 4 * (int64_t)ssim6_groups(W);
+  if (want_ssim && W >= kSsimTaps && (int64_t)ssim7_strips(W) > nstrips) nstrips = ssim7_strips(W);
   return (size_t)(n_cubes * T * nstrips * 2 * C) * sizeof(double);
 }
 
@@ -248,14 +227,16 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, 
   const bool ssim = want_ssim != 0;
   a.TX = eval_tx(C, ssim);
   a.nstrips = (int)((W + a.TX - 1) / a.TX);
-  // vertical-first SSIM kernel: frames, float32 original, no PCA, 4-byte aligned frame rows
-  a.ssim6 = ssim && frames && odtype == CV_F32 && W % 4 == 0 && !getenv("CVB_SSIM_V5") &&
-            (!pca || (fdtype == CV_U16 && E <= k6PcaMax));
-  if (a.ssim6) a.nstrips = 4 * ssim6_groups(W);
+  // the SSIM kernel with bulk-copied rows: frames, float32 original, 16-byte
+  // aligned rows (original W*C*4 and frame W*b bytes), <= 12 PCA planes
+  const int fsz = fdtype == CV_U8 ? 1 : 2;
+  a.ssim7 = ssim && frames && odtype == CV_F32 && (W * C) % 4 == 0 && (W * fsz) % 16 == 0 &&
+            ((uintptr_t)orig % 16) == 0 && ((uintptr_t)frames % 16) == 0 && (!pca || E <= k7PcaMax);
+  if (a.ssim7) a.nstrips = ssim7_strips(W);
   // streaming PSNR-only kernel: frames, f32/u16 original, no PCA, C in {4, 7},
   // 4-pixel quads; nstrips = pixel chunks per frame (<= the workspace's strips)
   a.psnr_vec = !ssim && frames && !pca && (odtype == CV_F32 || odtype == CV_U16) && (C == 4 || C == 7) &&
-               (H * W) % 4 == 0 && !getenv("CVB_PSNR_ROWS");
+               (H * W) % 4 == 0;
   if (a.psnr_vec) {
     const int64_t want = (H * W + 32767) / 32768;  // ~32 K pixels per CTA
     a.nstrips = (int)(want < a.nstrips ? want : a.nstrips);

@@ -35,7 +35,7 @@ struct EvalArgs {
   double *part;  // [n][T][nstrips][2C]
   uint32_t *err;
   int TX, nstrips;
-  int ssim6;  // launch k_eval_ssim6 (nstrips = 4 * ssim6_groups(W))
+  int ssim7;  // launch k_eval_ssim7 (nstrips = ssim7_strips(W))
   int psnr_vec;  // launch k_eval_psnr (nstrips = pixel chunks per frame)
 };
 

@@ -433,3 +433,53 @@ def test_gram_kernels_ragged(cuda, monkeypatch, C, n_pix, variant):
     assert np.all(np.abs(out[C:].reshape(C, C) - want_G) <= 1e-10 * scale + 1e-300)
     np.testing.assert_array_equal(g["mins"].cpu().numpy(), x.min(axis=0).astype(np.float64))
     np.testing.assert_array_equal(g["maxs"].cpu().numpy(), x.max(axis=0).astype(np.float64))
+
+
+# ------------------------------------------------------------------ bulk-copy SSIM kernel edge cases
+
+@pytest.mark.parametrize("shape,bits,n_pcs,noisy", [
+    ((3, 11, 256, 7), 10, 0, False),     # minimum height, 3 strips, partial last strip, band groups 4+3
+    ((2, 37, 128, 5), 8, 0, True),       # odd H, u8 frames (W % 16), groups 4+1, noisy frames
+    ((2, 24, 240, 4), 12, 0, False),     # 12-bit without PCA (exact float64 dequantisation), C % 4 == 0
+    ((2, 19, 136, 12), 16, 6, True),     # PCA 12->6, three band groups, odd H
+    ((2, 16, 64, 12), 12, 9, False),     # PCA 12->9
+    ((1, 21, 128, 8), 8, 5, False),      # 8-bit PCA planes, generic plane count
+])
+def test_ssim_bulk_kernel_shapes(cuda, shape, bits, n_pcs, noisy):
+    rng = np.random.default_rng(sum(shape) + bits)
+    T, H, W, C = shape
+    yy, xx = np.mgrid[0:H, 0:W]
+    base = np.stack([np.sin(yy / (3 + c) + xx / (5 + 2 * c)) for c in range(C)], -1)
+    x = (base[None] * (1 + np.arange(C)) + 0.3 * rng.normal(size=shape)).astype(np.float32)
+    if n_pcs == 0:
+        x[rng.random(shape) < 0.05] = np.nan
+    spec = G_pipe.StreamSpec(bits, n_pcs=n_pcs)
+    xt = torch.from_numpy(x).to(cuda)
+    enc = G_pipe.encode_prep(xt, spec)
+    enc.check()
+    ref = O.encode_stream(x, bits, n_pcs=n_pcs)
+    frames_o = ref["frames"]
+    if n_pcs == 0:
+        np.testing.assert_array_equal(enc.frames[0].cpu().numpy(), frames_o)
+    if noisy:
+        frames_o = O.decoded_frames_with_noise(frames_o, bits)
+    # decode the oracle's frames so that only the decode+metric path is compared
+    fr = torch.from_numpy(frames_o[None]).to(cuda)
+    if n_pcs:
+        enc.qmins.copy_(torch.from_numpy(np.asarray(ref["mins"])[None]))
+        enc.qmaxs.copy_(torch.from_numpy(np.asarray(ref["maxs"])[None]))
+        mean_o, comps_o, ev_o = ref["pca"]
+        m = G.PcaModel(mean_o, comps_o, ev_o, n_input_channels=C)
+        enc.pca[0] = G_pipe._fold(m)
+    recon, sc = G_pipe.decode_eval(enc, xt, frames=fr)
+    rec_o = O.decode_stream(frames_o, ref, x.shape, bits)
+    if n_pcs == 0:
+        np.testing.assert_array_equal(recon.cpu().numpy(), rec_o.astype(np.float32))
+    else:
+        np.testing.assert_allclose(recon.cpu().numpy(), rec_o, rtol=1e-5, atol=1e-5 * np.abs(rec_o).max())
+    rep = sc.report()[0]
+    np.testing.assert_allclose(rep["psnr_per_band"], M.psnr_per_band(ref["filled"], rec_o), atol=PSNR_TOL_DB)
+    np.testing.assert_allclose(rep["ssim_per_band"], M.ssim_per_band(ref["filled"], rec_o), atol=SSIM_TOL)
+    # no recon output requested: same scores
+    _, sc2 = G_pipe.decode_eval(enc, xt, frames=fr, want_recon=False)
+    np.testing.assert_allclose(sc2.report()[0]["ssim_per_band"], rep["ssim_per_band"], rtol=0, atol=1e-12)
