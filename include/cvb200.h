@@ -68,6 +68,11 @@ const char *cv_last_error(void);
 int cv_max_channels(void);
 /* number of kernels this library has launched in the process (benchmark accounting) */
 unsigned long long cv_launch_count(void);
+/* Select a kernel variant for A/B measurements and tests (process-wide; set it
+ * before launching, not concurrently with launches). Names: "gram_tiles" (0/1),
+ * "gram_nt" (64 or 256), "proj_nopf" (0/1), "qp_px1" (0/1), "qp_runtime_c" (0/1).
+ * Defaults are the measured-fastest variants. Unknown names / values: CV_ERR_ARG. */
+int cv_set_variant(const char *name, int value);
 
 /* ---------------------------------------------------------------------- */
 /* K1 — per-band statistics (+ forward-fill segment carries)               */

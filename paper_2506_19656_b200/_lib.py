@@ -37,6 +37,7 @@ SIGNATURES = {
     "cv_last_error": ([], ctypes.c_char_p),
     "cv_max_channels": ([], _INT),
     "cv_launch_count": ([], ctypes.c_ulonglong),
+    "cv_set_variant": ([ctypes.c_char_p, _INT], _INT),
     "cv_stats_ws_bytes": ([_I64, _I32], _SZ),
     "cv_num_segments": ([_I64, _I32], _I64),
     "cv_stats_reset": ([_P, _I64, _I32, _P], _INT),
@@ -99,3 +100,8 @@ def check(status: int, what: str) -> None:
 def call(name: str, *args) -> None:
     fn = getattr(load(), name)
     check(fn(*args), name)
+
+
+def set_variant(name: str, value: int) -> None:
+    """Select a kernel variant (A/B measurements, tests); see cv_set_variant."""
+    check(load().cv_set_variant(name.encode(), int(value)), "cv_set_variant")

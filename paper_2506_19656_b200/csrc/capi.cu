@@ -8,6 +8,7 @@
 namespace cvb {
 
 static thread_local std::string g_last_error;
+Variants g_variants;
 // kernels launched through this library (every launch site calls check_launch once)
 static std::atomic<unsigned long long> g_launches{0};
 
@@ -50,6 +51,21 @@ const char *cv_status_string(int status) {
 const char *cv_last_error(void) { return cvb::g_last_error.c_str(); }
 
 int cv_max_channels(void) { return cvb::kMaxC; }
+
+int cv_set_variant(const char *name, int value) {
+  if (!name) return cvb::fail(CV_ERR_ARG, "cv_set_variant: null name");
+  const std::string n(name);
+  cvb::Variants &v = cvb::g_variants;
+  if (n == "gram_tiles") v.gram_tiles = value != 0;
+  else if (n == "gram_nt") {
+    if (value != 64 && value != 256) return cvb::fail(CV_ERR_ARG, "gram_nt must be 64 or 256, got %d", value);
+    v.gram_nt = value;
+  } else if (n == "proj_nopf") v.proj_nopf = value != 0;
+  else if (n == "qp_px1") v.qp_px1 = value != 0;
+  else if (n == "qp_runtime_c") v.qp_runtime_c = value != 0;
+  else return cvb::fail(CV_ERR_ARG, "cv_set_variant: unknown variant '%s'", name);
+  return CV_OK;
+}
 
 unsigned long long cv_launch_count(void) { return cvb::g_launches.load(std::memory_order_relaxed); }
 

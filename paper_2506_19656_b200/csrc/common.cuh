@@ -17,6 +17,17 @@ void set_last_error(const std::string &msg);
 int fail(int status, const char *fmt, ...);
 int check_launch(const char *what);
 
+// Kernel-variant selection for A/B measurements and tests (cv_set_variant);
+// plain ints read by the launchers, never the environment.
+struct Variants {
+  int gram_tiles = 0;    // 1: tiled k_gram instead of the pixel-per-lane k_gram_px
+  int gram_nt = 64;      // k_gram_px CTA size: 64 or 256
+  int proj_nopf = 0;     // 1: no next-pixel prefetch in k_pca_project_px (C = 12)
+  int qp_px1 = 0;        // 1: one pixel per thread in k_quantize_planar
+  int qp_runtime_c = 0;  // 1: runtime band count for the C = 12 PCA quantiser
+};
+extern Variants g_variants;
+
 // ----------------------------------------------------------------- limits
 constexpr int kMaxC = 32;        // channels per stream handled by one CTA row
 constexpr int kSsimRadius = 5;   // 11x11 window

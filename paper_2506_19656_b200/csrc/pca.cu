@@ -609,11 +609,10 @@ template <typename TIn>
 static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *out, void *stats,
                        uint32_t *err, cudaStream_t st) {
   if constexpr (std::is_same<TIn, float>::value) {
-    if (C <= kGpxC && ((uintptr_t)src & 15) == 0 && !getenv("CVB_GRAM_TILES")) {
+    if (C <= kGpxC && ((uintptr_t)src & 15) == 0 && !g_variants.gram_tiles) {
       int nblk = gram_blocks(n_pix, C);
       if (nblk > num_sms()) nblk = num_sms();
-      const char *ntv = getenv("CVB_GRAM_NT");
-      const int NT = ntv ? atoi(ntv) : 64;
+      const int NT = g_variants.gram_nt == 256 ? 256 : 64;
       if (NT == 64) nblk = (int)min((int64_t)gram_blocks(n_pix, C), (int64_t)5 * num_sms());
       size_t sm = (size_t)kGpxS * NT * C * sizeof(float);
       const size_t smr = (size_t)(NT / 64) * (kGpxNP + kGpxC) * sizeof(double);
@@ -666,9 +665,9 @@ static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const
       if (nb1 > 2 * cap) nb1 = 2 * cap;
       dim3 grid1((unsigned)(nb1 < 1 ? 1 : nb1), (unsigned)n_cubes);
       if (p.K <= 8)
-        k_pca_project_px<TIn, TO, 8, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err, getenv("CVB_PROJ_NOPF") != nullptr);
+        k_pca_project_px<TIn, TO, 8, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err, g_variants.proj_nopf != 0);
       else
-        k_pca_project_px<TIn, TO, 12, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err, getenv("CVB_PROJ_NOPF") != nullptr);
+        k_pca_project_px<TIn, TO, 12, 12, 1><<<grid1, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err, g_variants.proj_nopf != 0);
     } else if (p.C <= 8) {
       if (p.K <= 8) CV_PX(8, 8); else CV_PX(16, 8);
     } else {

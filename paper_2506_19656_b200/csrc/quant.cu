@@ -380,7 +380,7 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
   constexpr int VE = 16 / sizeof(TIn);
   // pixel pairs with register-resident band constants (the common case)
   const bool px2 = (PCA ? (args.C <= kQPcaC && args.E <= kQPcaC) : args.C <= kQRegC) && args.HW % 2 == 0 &&
-                   !getenv("CVB_QP_PX1");
+                   !g_variants.qp_px1;
   const int NT = px2 ? 128 : 256;
   const int P = px2 ? 2 * NT : NT;
   const int NE = P * args.C;
@@ -395,7 +395,7 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
   } while (0)
-  if (px2 && PCA && args.C == 12 && mv <= 8 && mv > 4 && !getenv("CVB_QP_RUNTIME_C")) {
+  if (px2 && PCA && args.C == 12 && mv <= 8 && mv > 4 && !g_variants.qp_runtime_c) {
     auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, 8, true, 12>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);

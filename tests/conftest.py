@@ -42,3 +42,19 @@ def cuda():
 
     _lib.load()
     return torch.device("cuda", 0)
+
+
+@pytest.fixture
+def variant_sel():
+    """Select kernel variants (cv_set_variant) for one test; restores the defaults."""
+    from paper_2506_19656_b200 import _lib
+
+    defaults = {"gram_tiles": 0, "gram_nt": 64, "proj_nopf": 0, "qp_px1": 0, "qp_runtime_c": 0}
+
+    def sel(variants: dict):
+        for k, v in variants.items():
+            _lib.set_variant(k, v)
+
+    yield sel
+    for k, v in defaults.items():
+        _lib.set_variant(k, v)

@@ -60,3 +60,15 @@ def test_validation_without_launch():
     assert lib.cv_stats_finalize(1, 0, 3, 0, 0.0, None, None, None, None) == _lib.CV_OK
     with pytest.raises(Exception):
         _lib.check(_lib.CV_ERR_ARG, "x")
+
+
+def test_set_variant_validation():
+    """Kernel-variant selection is host-only state: unknown names and CTA sizes
+    the launcher has no instantiation for are rejected (gram_nt=128)."""
+    lib = _lib.load()
+    assert lib.cv_set_variant(b"gram_nt", 128) == _lib.CV_ERR_ARG
+    assert b"64 or 256" in lib.cv_last_error()
+    assert lib.cv_set_variant(b"no_such_knob", 1) == _lib.CV_ERR_ARG
+    for name, default in (("gram_nt", 64), ("gram_tiles", 0), ("proj_nopf", 0), ("qp_px1", 0),
+                          ("qp_runtime_c", 0)):
+        assert lib.cv_set_variant(name.encode(), default) == _lib.CV_OK

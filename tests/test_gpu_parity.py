@@ -410,14 +410,13 @@ def test_psnr_stream_kernel(cuda, shape, B, u16):
 
 @pytest.mark.parametrize("C", [1, 5, 7, 12])
 @pytest.mark.parametrize("n_pix", [1, 63, 64 * 5 + 3, 100_003])
-@pytest.mark.parametrize("variant", [{}, {"CVB_GRAM_NT": "256"}, {"CVB_GRAM_TILES": "1"}])
-def test_gram_kernels_ragged(cuda, monkeypatch, C, n_pix, variant):
+@pytest.mark.parametrize("variant", [{}, {"gram_nt": 256}, {"gram_tiles": 1}])
+def test_gram_kernels_ragged(cuda, variant_sel, C, n_pix, variant):
     """k_gram_px (64- and 256-thread CTAs) and the tiled k_gram against a float64
     numpy shifted Gram (transform.py:177-179 restated as one-pass sums): ragged
     pixel counts, C below the 12-band register width; band extremes bit-exact."""
     from paper_2506_19656_b200 import _device as dev
-    for k, v in variant.items():
-        monkeypatch.setenv(k, v)
+    variant_sel(variant)
     rng = np.random.default_rng(1000 * C + n_pix % 997)
     x = (rng.standard_normal((n_pix, C)) * 10.0 ** np.arange(C) / 7 + 3.0).astype(np.float32)
     arr = dev.to_device(x)
@@ -483,3 +482,23 @@ def test_ssim_bulk_kernel_shapes(cuda, shape, bits, n_pcs, noisy):
     # no recon output requested: same scores
     _, sc2 = G_pipe.decode_eval(enc, xt, frames=fr, want_recon=False)
     np.testing.assert_allclose(sc2.report()[0]["ssim_per_band"], rep["ssim_per_band"], rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------------ kernel variants agree bit for bit
+
+@pytest.mark.parametrize("variant", [{"qp_runtime_c": 1}, {"qp_px1": 1}, {"proj_nopf": 1}])
+@pytest.mark.parametrize("shape,n_pcs,bits", [((3, 40, 72, 12), 6, 16), ((2, 33, 64, 12), 9, 12)])
+def test_pca_variants_bit_identical(cuda, variant_sel, variant, shape, n_pcs, bits):
+    """The compile-time C = 12 PCA quantiser, the pixel-pair path and the prefetching
+    projection produce exactly the frames / ranges of their generic counterparts
+    (the 1-LSB parity bar cannot see a divergence between them)."""
+    from paper_2506_19656_b200 import synth
+
+    x = synth.era5(49656, shape, device=cuda)
+    spec = G_pipe.StreamSpec(bits, n_pcs=n_pcs, normalize=True)
+    a = G_pipe.encode_prep(x, spec)
+    fa, ma = a.frames.clone(), a.qmins.clone()
+    variant_sel(variant)
+    b = G_pipe.encode_prep(x, spec)
+    assert torch.equal(b.qmins, ma) and torch.equal(b.qmaxs, a.qmaxs)
+    assert torch.equal(b.frames, fa)
