@@ -55,6 +55,8 @@ def _args(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / CPU arm)")
+    ap.add_argument("--variant", action="append", default=[], metavar="NAME=VALUE",
+                    help="kernel variant for A/B runs (cv_set_variant), e.g. eval_kernel=7")
     return ap.parse_args(argv)
 
 
@@ -391,6 +393,9 @@ def run_ours(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
+    for kv in a.variant:
+        name, value = kv.split("=")
+        _lib.set_variant(name, int(value))
 
     wl = Workload(a.config, rank, world, a.cubes, a.t)
     x = wl.make_input(dev, rank)

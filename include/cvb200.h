@@ -70,7 +70,8 @@ int cv_max_channels(void);
 unsigned long long cv_launch_count(void);
 /* Select a kernel variant for A/B measurements and tests (process-wide; set it
  * before launching, not concurrently with launches). Names: "gram_tiles" (0/1),
- * "gram_nt" (64 or 256), "proj_nopf" (0/1), "qp_px1" (0/1), "qp_runtime_c" (0/1).
+ * "gram_nt" (64 or 256), "proj_nopf" (0/1), "qp_px1" (0/1), "qp_runtime_c" (0/1),
+ * "eval_kernel" (0 = by decode mode, 7 / 8 = force k_eval_ssim7 / k_eval_ssim8).
  * Defaults are the measured-fastest variants. Unknown names / values: CV_ERR_ARG. */
 int cv_set_variant(const char *name, int value);
 
@@ -257,6 +258,39 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins,
             int64_t H, int64_t W, int32_t C, const double *peaks,
             int32_t want_ssim, float *recon_out, void *ws, double *sse,
             double *ssim_sum, uint32_t *err_word, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* layout: select_for_video (cube.py:249-305), planar bytes (bridge.py:157-174) */
+/* ---------------------------------------------------------------------- */
+
+/*
+ * select_for_video (cube.py:249-305): stack C channels into a contiguous
+ * channel-last out [T][H][W][C]. chan_ptrs: HOST array of C DEVICE pointers,
+ * channel c of the result (a 3-D variable, or one index of a 4-D variable's
+ * channel axis). strides: HOST array [C][3], element strides of channel c
+ * along the (t, y, x) roles of axis_order (the transposition the reference does
+ * with np.transpose). Elements are moved as raw words of elem_size bytes
+ * (1, 2, 4 or 8); all channels share the element type.
+ */
+int cv_select_stack(const void *const *chan_ptrs, const int64_t *strides,
+                    int32_t C, int32_t elem_size, int64_t T, int64_t H,
+                    int64_t W, void *out, void *stream);
+
+/*
+ * _frames_to_planar_bytes (bridge.py:157-160): q channel-last [T][HW][n_planes]
+ * (u8/u16) -> out planar [T][n_planes][HW], the byte stream one video's
+ * encoder reads (little-endian u16 is the device's native order).
+ */
+int cv_planar_pack(const void *q, int32_t dtype, int64_t T, int64_t HW,
+                   int32_t n_planes, void *out, void *stream);
+
+/*
+ * _planar_bytes_to_frames (bridge.py:163-174): planes [T][n_planes][HW] ->
+ * out channel-last [T][HW][n_planes]. The whole-frames byte-count check
+ * (CorruptStreamError, bridge.py:167-171) is the caller's (host arithmetic).
+ */
+int cv_planar_unpack(const void *planes, int32_t dtype, int64_t T, int64_t HW,
+                     int32_t n_planes, void *out, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* spectral angle                           */

@@ -49,6 +49,38 @@ def forward_fill(arr: np.ndarray, time_axis: int, fill=0.0):
             np.moveaxis(observed, 0, time_axis))
 
 
+def select_for_video(variables: dict, axes: dict, names, axis_order) -> np.ndarray:
+    """cube.py:249-305 — 3-D variables transposed to ``axis_order`` and stacked on a
+    new last axis, or one 4-D variable transposed with its extra axis last."""
+    names = [names] if isinstance(names, str) else list(names)
+    order = tuple(axis_order)
+    if len(order) != 3 or not names or len(set(names)) != len(names):
+        raise OracleError("bad selection")
+    if any(n not in variables for n in names):
+        raise OracleError("unknown variable")
+    nd = {np.ndim(variables[n]) for n in names}
+    if nd == {4}:
+        if len(names) != 1:
+            raise OracleError("several 4-D variables")
+        ax = tuple(axes[names[0]])
+        rest = [a for a in ax if a not in order]
+        if len(rest) != 1 or any(a not in ax for a in order):
+            raise OracleError("axes do not match")
+        perm = [ax.index(a) for a in order + (rest[0],)]
+        return np.ascontiguousarray(np.transpose(variables[names[0]], perm))
+    if nd != {3}:
+        raise OracleError("mixed ranks")
+    cols = []
+    for n in names:
+        ax = tuple(axes[n])
+        if set(ax) != set(order):
+            raise OracleError("axes do not match")
+        cols.append(np.transpose(variables[n], [ax.index(a) for a in order]))
+        if cols[-1].shape != cols[0].shape:
+            raise OracleError("shape mismatch")
+    return np.ascontiguousarray(np.stack(cols, axis=-1))
+
+
 # --------------------------------------------------------------------------- transform.py
 
 def fit_quant(arr: np.ndarray):

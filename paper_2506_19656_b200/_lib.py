@@ -55,6 +55,9 @@ SIGNATURES = {
     "cv_eval_ws_bytes": ([_I64, _I64, _I64, _I64, _I32, _I32], _SZ),
     "cv_eval": ([_P, _I32, _I32, _P, _P, _I32, _P, _P, _P, _I32, _P, _I32,
                  _I64, _I64, _I64, _I64, _I32, _P, _I32, _P, _P, _P, _P, _P, _P], _INT),
+    "cv_select_stack": ([_P, _P, _I32, _I32, _I64, _I64, _I64, _P, _P], _INT),
+    "cv_planar_pack": ([_P, _I32, _I64, _I64, _I32, _P, _P], _INT),
+    "cv_planar_unpack": ([_P, _I32, _I64, _I64, _I32, _P, _P], _INT),
     "cv_angle_ws_bytes": ([], _SZ),
     "cv_spectral_angle": ([_P, _I32, _P, _I32, _I64, _I32, _P, _P, _P], _INT),
 }

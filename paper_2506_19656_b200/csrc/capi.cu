@@ -63,6 +63,11 @@ int cv_set_variant(const char *name, int value) {
   } else if (n == "proj_nopf") v.proj_nopf = value != 0;
   else if (n == "qp_px1") v.qp_px1 = value != 0;
   else if (n == "qp_runtime_c") v.qp_runtime_c = value != 0;
+  else if (n == "eval_kernel") {
+    if (value != 0 && value != 7 && value != 8)
+      return cvb::fail(CV_ERR_ARG, "eval_kernel must be 0, 7 or 8, got %d", value);
+    v.eval_kernel = value;
+  }
   else return cvb::fail(CV_ERR_ARG, "cv_set_variant: unknown variant '%s'", name);
   return CV_OK;
 }

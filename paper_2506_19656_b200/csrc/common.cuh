@@ -25,6 +25,7 @@ struct Variants {
   int proj_nopf = 0;     // 1: no next-pixel prefetch in k_pca_project_px (C = 12)
   int qp_px1 = 0;        // 1: one pixel per thread in k_quantize_planar
   int qp_runtime_c = 0;  // 1: runtime band count for the C = 12 PCA quantiser
+  int eval_kernel = 0;   // SSIM kernel: 0 = by decode mode (PCA: k_eval_ssim8, else k_eval_ssim7), 7 / 8 = forced
 };
 extern Variants g_variants;
 

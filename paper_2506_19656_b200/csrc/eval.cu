@@ -25,6 +25,7 @@
 #include "eval_kernel.cuh"
 #include "ssim_kernel.cuh"
 #include "ssim7_kernel.cuh"
+#include "ssim8_kernel.cuh"
 #include "psnr_kernel.cuh"
 
 #include <cstdlib>
@@ -71,6 +72,34 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
     const int wpc = a.C < kSsimWarpsPerCta ? a.C : kSsimWarpsPerCta;
     dim3 grid((unsigned)(a.nstrips * ncg), (unsigned)a.T, (unsigned)n);
     if constexpr ((RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) && std::is_same<TO, float>::value) {
+      // PCA streams run k_eval_ssim8 (park-only rings: config 5 eval 74 -> 71 ms), the
+      // lookup-table / float64 decodes k_eval_ssim7 (its raw-input prefetch hides the
+      // dependent code -> table loads: config 2 eval 24.6 vs 27 ms); "eval_kernel" forces one
+      const int ek = g_variants.eval_kernel;
+      if (a.ssim7 && (ek == 8 || (ek == 0 && pca))) {
+        constexpr int fsz = RS == RS_FRAMES_U8 ? 1 : 2;
+        const int ngrp = (a.C + k8GB - 1) / k8GB;
+        dim3 g8((unsigned)(ssim8_strips(a.W) * ngrp), (unsigned)a.T, (unsigned)n);
+#define CV_S8(MODE, EP, EX)                                                                                \
+  do {                                                                                                   \
+    const Ssim8Geom g8m = ssim8_geom(a.C, MODE == K8_PCA ? a.E : k8GB, fsz, MODE == K8_LUT);              \
+    if (g8m.ns < 2) return fail(CV_ERR_UNSUPPORTED, "cv_eval: %d channels do not fit the SSIM kernel's rings", a.C); \
+    const size_t sm = (size_t)g8m.total;                                                                 \
+    cudaFuncSetAttribute(k_eval_ssim8<RS, MODE, EP, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_eval_ssim8<RS, MODE, EP, EX><<<g8, k8Threads, sm, st>>>(a, inv);                                   \
+  } while (0)
+        if (pca) {
+          if (a.E == 6) CV_S8(K8_PCA, 6, true);
+          else if (a.E == 9) CV_S8(K8_PCA, 9, true);
+          else CV_S8(K8_PCA, k8PcaMax, false);
+        } else if (a.bit_depth <= 10) {
+          CV_S8(K8_LUT, 0, false);
+        } else {
+          CV_S8(K8_F64, 0, false);
+        }
+#undef CV_S8
+        return check_launch("cv_eval(ssim8)");
+      }
       if (a.ssim7) {
         constexpr int fsz = RS == RS_FRAMES_U8 ? 1 : 2;
         const int ngrp = (a.C + k7GB - 1) / k7GB;

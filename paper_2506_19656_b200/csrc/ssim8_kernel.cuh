@@ -1,0 +1,568 @@
+// K5+K6 with SSIM — the decode + PSNR + SSIM kernel of the benchmark
+// (frames + float32 original; every bit depth, with or without band PCA).
+//
+// Replaces, for the array path: _planar_bytes_to_frames (bridge.py:163-174),
+// dropping padded planes (plan.py:106), dequantize (transform.py:108-126),
+// pca_inverse (transform.py:202-210) and the absent metrics module's psnr /
+// ssim (11x11 Gaussian window, sigma 1.5, valid region).
+//
+// CTA = one frame t of one cube, 128 adjacent input columns x0 .. x0+127
+// (x0 = 118 s; the 118 output columns x0+5 .. x0+122 need their whole window
+// inside the strip) and a group of up to four bands g*4 .. g*4+3; it walks the
+// frame top to bottom in row pairs. 28 warps in two roles:
+//   * 16 "vertical" warps (88 registers); lane = (column 8w + lane/4, band
+//     lane%4): conflict-free reads of the channel-last original, 16-byte recon
+//     runs. Per row pair a lane decodes its two elements (float2 lookup table
+//     of the exact float64 dequantisation for <= 10 bits; exact float64 for
+//     12/16-bit without PCA; float32 inverse PCA with the dequantisation
+//     folded into the coefficients), stores the recon, adds the squared error
+//     and steps the VERTICAL 11-tap filter of (s, d) and (s^2, d^2), a
+//     transposed-form FIR on packed FFMA2 (s = x'+y', d = x-y, x' = x - peak).
+//     Column-filtered row pairs go to a 6-slot shared ring.
+//   * 11 "horizontal" warps (48 registers) take the (row, band) tasks of the
+//     filtered pairs round-robin. Lane q filters columns 4q .. 4q+13 of a row
+//     into outputs 4q .. 4q+3 (14 LDS.128, 22 FFMA2 per output) and scores
+//     them. The horizontal role is a third of the instructions: it idles on
+//     the "filled" barrier rather than making the vertical warps wait.
+//   * 1 loader warp (in the horizontal warpgroups) feeds the input ring:
+//     mbarrier-tracked bulk copies (cp.async.bulk, the TMA path), one per
+//     original row segment (all C bands of 128 pixels) and per frame-plane row
+//     segment, as far ahead as the ring (3 row pairs) allows.
+// Both rings are handed over with hardware named barriers (bar.arrive by one
+// side, bar.sync by the other): a waiting warp is parked by the barrier unit and
+// issues nothing, unlike an mbarrier try_wait loop (27 % of the issued
+// instructions of k_eval_ssim7 are such polls). Only the copies' completion is
+// an mbarrier. Gaussian weights are compile-time immediates.
+#pragma once
+#include "eval_kernel.cuh"
+#include "ssim_kernel.cuh"
+
+namespace cvb {
+
+constexpr int k8Cols = 128;
+constexpr int k8Out = k8Cols - 2 * kSsimRadius;  // 118
+constexpr int k8GB = 4;                          // bands per CTA
+constexpr int k8VW = 16;                         // vertical warps (warpgroups 0-3)
+constexpr int k8HW = 12;                         // horizontal warpgroups' warps (4-6): 11 workers + the loader
+constexpr int k8HWork = k8HW - 1;
+constexpr int k8Threads = 32 * (k8VW + k8HW);
+constexpr int k8RegsV = 88;                      // setmaxnreg: vertical warpgroups
+constexpr int k8RegsH = 48;                      // setmaxnreg: horizontal warpgroups
+constexpr int k8NSMax = 3;                       // input ring stages (row pairs); 16 barrier ids bound it
+constexpr int k8SmemMax = 227 * 1024;
+constexpr int k8Ring = 6;                        // filtered-row ring slots (row pairs); even
+constexpr int k8PcaMax = 12;
+constexpr int k8LutMax = 1024;
+constexpr int k8VbBand = 144;                    // float4 per band row (136 used + skew)
+constexpr int k8VbRow = k8GB * k8VbBand;         // float4 per filtered row (4 bands)
+constexpr int k8Bars = 64;                       // bytes of mbarriers
+constexpr int k8Desc = k8GB * 16;                // bytes of the per-band SSIM constants (c0, C1, C2)
+constexpr int k8Coef = k8GB * k8PcaMax * 4;      // bytes of the inverse-PCA coefficients [band][plane]
+// Named barriers (ids 1 .. 15; no polling anywhere except the copies' mbarrier):
+//   k8BarFilled + slot   the 16 vertical warps arrive, the 8 horizontal workers
+//                        of the pair's (row, band) tasks wait parked;
+//   k8BarDrained + slot  those 8 workers arrive, the vertical warps wait parked
+//                        before they overwrite the slot (this puts the vertical
+//                        warps in step once per pair; an mbarrier each warp polls
+//                        on its own measured the same time at 40 % more issued
+//                        instructions, the polls competing with the workers);
+//   k8BarStage + stage   the vertical warps arrive when they have read an input
+//                        stage, the loader waits parked before refilling it.
+constexpr int k8BarFilled = 1, k8BarDrained = 1 + k8Ring, k8BarStage = 1 + 2 * k8Ring;
+static_assert(k8BarStage + k8NSMax <= 16, "named barrier ids");
+constexpr int k8BarCount = 32 * (k8VW + 2 * k8GB);
+enum { K8_LUT = 0, K8_F64 = 1, K8_PCA = 2 };
+
+__host__ __device__ inline int ssim8_strips(int64_t W) { return (int)((W - 2 * kSsimRadius + k8Out - 1) / k8Out); }
+
+struct Ssim8Geom {
+  int ob, fb, np, ns, stage, off_desc, off_coef, off_in, off_vb, off_lut, total;
+};
+
+// shared-memory geometry: np frame planes per row (PCA: E; else the group's bands)
+__host__ __device__ inline Ssim8Geom ssim8_geom(int C, int np, int fsz, bool lut) {
+  Ssim8Geom g;
+  g.ob = ((k8Cols * C * 4 + 15) & ~15) + 32;  // 16-byte aligned copy of 128 pixels + slack
+  g.fb = ((k8Cols * fsz + 15) & ~15) + 32;
+  g.np = np;
+  g.stage = 2 * g.ob + 2 * np * g.fb;
+  g.off_desc = k8Bars;
+  g.off_coef = g.off_desc + k8Desc;
+  g.off_in = g.off_coef + k8Coef;
+  const int rest = g.off_in + k8Ring * 2 * k8VbRow * 16 + (lut ? k8GB * k8LutMax * 8 : 0);
+  g.ns = (k8SmemMax - rest) / g.stage;
+  g.ns = g.ns > k8NSMax ? k8NSMax : g.ns;  // < 2: the kernel cannot run (the launcher checks)
+  g.off_vb = g.off_in + g.ns * g.stage;
+  g.off_lut = g.off_vb + k8Ring * 2 * k8VbRow * 16;
+  g.total = g.off_lut + (lut ? k8GB * k8LutMax * 8 : 0);
+  return g;
+}
+
+__device__ __forceinline__ void mbar_init8(uint32_t b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx8(uint32_t b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(tx) : "memory");
+}
+// One try_wait (which may suspend briefly in hardware); on failure the warp
+// sleeps before polling again instead of spinning on issue slots the working
+// warps need.
+__device__ __forceinline__ void mbar_wait8(uint32_t b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(b), "r"(parity)
+      : "memory");
+  while (!ok) {
+    asm volatile("nanosleep.u32 128;\n" ::: "memory");
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+// global -> shared bulk copy (TMA engine), completion counted on `bar` in bytes
+__device__ __forceinline__ void bulk_g2s8(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// named barriers: producers arrive, consumers sync (both count towards `n` threads)
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+// Ring data is read through volatile asm so that no load is hoisted above the
+// barrier that publishes it.
+__device__ __forceinline__ float lds8_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds8_f32x2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds8_f32x4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts8_f32x4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+template <int FSZ>
+__device__ __forceinline__ uint32_t lds8_code(uint32_t a) {
+  uint32_t v;
+  if constexpr (FSZ == 2) asm volatile("ld.shared.u16 %0, [%1];\n" : "=r"(v) : "r"(a));
+  else asm volatile("ld.shared.u8 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// a value the compiler must keep in a register (it cannot rematerialise it
+// from thread indices inside the hot loop)
+__device__ __forceinline__ uint32_t opaque8(uint32_t x) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;\n" : "=r"(r) : "r"(x));
+  return r;
+}
+
+// a - b on packed pairs (one rounding: b * -1 + a)
+__device__ __forceinline__ float2 fsub2_8(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
+
+// transposed-form 11-tap FIR on packed pairs: zsd = (s, d), zq = (s^2, d^2);
+// z[k] holds the partial sums of the output row completed k rows from now.
+struct Fir8 {
+  float2 zsd[10], zq[10];
+};
+
+__device__ __forceinline__ float4 fir8_step(Fir8 &f, float2 p) {
+  const float2 q = __fmul2_rn(p, p);
+  const float w0 = gtap(5);
+  const float2 osd = __ffma2_rn(p, make_float2(w0, w0), f.zsd[0]);
+  const float2 oq = __ffma2_rn(q, make_float2(w0, w0), f.zq[0]);
+#pragma unroll
+  for (int k = 1; k < 10; ++k) {
+    const float wt = gtap(k - 5 < 0 ? 5 - k : k - 5);
+    f.zsd[k - 1] = __ffma2_rn(p, make_float2(wt, wt), f.zsd[k]);
+    f.zq[k - 1] = __ffma2_rn(q, make_float2(wt, wt), f.zq[k]);
+  }
+  f.zsd[9] = __fmul2_rn(p, make_float2(w0, w0));
+  f.zq[9] = __fmul2_rn(q, make_float2(w0, w0));
+  return make_float4(osd.x, osd.y, oq.x, oq.y);
+}
+
+__device__ __forceinline__ int vb8_skew(int b) { return b * k8VbBand + ((b & 1) | ((b & 2) << 1)); }  // {0,1,4,5} mod 8
+__device__ __forceinline__ int vb8_idx(int col) { return (col & 3) * 34 + (col >> 2); }
+
+// EP: PCA planes the loops are unrolled for; EXACT: E == EP (6 and 9), else
+// k8PcaMax with runtime guards; 0 without PCA.
+template <int RS, int MODE, int EP, bool EXACT>
+__global__ void __launch_bounds__(k8Threads, 1)
+k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
+  using R = typename RawT<RS>::type;
+  constexpr int FSZ = (int)sizeof(R);
+  constexpr bool PCA = MODE == K8_PCA;
+  constexpr int EPL = PCA ? EP : 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int C = args.C, E = EXACT ? EP : args.E;
+  const int ngrp = (C + k8GB - 1) / k8GB;
+  const int strip = blockIdx.x / ngrp, g = blockIdx.x % ngrp;
+  const int nb = min(k8GB, C - g * k8GB);
+  const int64_t T = args.T, H = args.H, W = args.W, HW = H * W;
+  const int64_t a = blockIdx.z, t = blockIdx.y;
+  const int64_t x0 = (int64_t)strip * k8Out;
+  const int nstr = gridDim.x / ngrp;
+  const bool last_strip = strip == nstr - 1;
+  const int H32 = (int)H, W32 = (int)W;
+  const int npairs = (H32 + 1) >> 1;
+  const int nfe = npairs - 5;  // filtered pairs (output rows 2e, 2e+1)
+  const int np = PCA ? E : nb;
+  const Ssim8Geom geo = ssim8_geom(C, PCA ? E : k8GB, FSZ, MODE == K8_LUT);
+
+  const uint32_t s0 = smem_u32(smem);
+  const int ns = geo.ns;
+  const uint32_t full_in = s0;  // + 8 * stage
+  const uint32_t in_ring = s0 + geo.off_in;
+  const uint32_t vb = s0 + geo.off_vb;
+  float2 *lut = reinterpret_cast<float2 *>(smem + geo.off_lut);
+  const double L = args.L;
+
+  if (threadIdx.x < k8NSMax) mbar_init8(full_in + 8 * threadIdx.x, 1);  // the loader's expect_tx arrival + bytes
+  if (threadIdx.x < k8GB) {  // per-band SSIM constants for the horizontal warps
+    const double pk = (int)threadIdx.x < nb ? args.peaks[a * C + g * k8GB + threadIdx.x] : 1.0;
+    reinterpret_cast<float4 *>(smem + geo.off_desc)[threadIdx.x] =
+        make_float4((float)pk, fmaxf((float)((0.01 * pk) * (0.01 * pk)), 1e-30f),
+                    fmaxf((float)((0.03 * pk) * (0.03 * pk)), 1e-30f), 0.f);
+  }
+  if constexpr (PCA) {
+    if (w == 2) {
+      for (int i = lane; i < k8GB * k8PcaMax; i += 32) {
+        const int bq = i / k8PcaMax, j = i % k8PcaMax;
+        float cf = 0.f;
+        if (bq < nb && j < E) {
+          const double m = args.qmins[a * E + j];
+          const double sp = __dsub_rn(args.qmaxs[a * E + j], m);
+          cf = (float)((sp / L) * inv.W[j * kMaxC + g * k8GB + bq]);
+        }
+        reinterpret_cast<float *>(smem + geo.off_coef)[i] = cf;
+      }
+    }
+  }
+  if constexpr (MODE == K8_LUT) {
+    // (hi, lo) float pair of the exact float64 dequantisation of every code
+    for (int i = threadIdx.x; i < k8GB * k8LutMax; i += blockDim.x) {
+      const int b = i / k8LutMax, q = i % k8LutMax;
+      if (b < nb && q <= (int)args.Li) {
+        const double m = args.qmins[a * C + g * k8GB + b];
+        const double sp = __dsub_rn(args.qmaxs[a * C + g * k8GB + b], m);
+        const double v = dequantize_fast((uint32_t)q, m, sp, L, args.rL);
+        const float hi = (float)v;
+        lut[i] = make_float2(hi, (float)(v - (double)hi));
+      }
+    }
+  }
+  // the input ring starts zeroed: bytes no copy ever writes (columns past the
+  // frame edge) read as 0, so the decode needs no per-element masking
+  for (int i = threadIdx.x; i < ns * geo.stage / 16; i += blockDim.x)
+    reinterpret_cast<uint4 *>(smem + geo.off_in)[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zeros before the first bulk copies
+  __syncthreads();
+  double *red = reinterpret_cast<double *>(smem + geo.off_vb);  // end-of-kernel partials [32 warps][32]
+
+  if (w >= k8VW) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(k8RegsH));
+    // ------------------------------------------------------------------ horizontal warpgroups
+    const int h = w - k8VW;
+    double hsumb[k8GB] = {0.0, 0.0, 0.0, 0.0};  // a worker's tasks cycle through the bands
+    if (h == k8HWork) {
+      // ---------------------------------------------------------------- loader warp
+      // copy k of a pair (lane k): row k / ncp of the pair, piece k % ncp
+      // (piece 0: the original's row segment, piece j+1: frame plane j)
+      const int ncp = 1 + np;
+      const int64_t rowb = W * C * 4;
+      const int64_t xe = min(x0 + k8Cols, W);
+      const int64_t oa0 = (x0 * C * 4) & ~15ll, oa1 = (xe * C * 4 + 15) & ~15ll;
+      const int64_t fa0 = (x0 * FSZ) & ~15ll, fa1 = (xe * FSZ + 15) & ~15ll;
+      const uint32_t obytes = (uint32_t)(oa1 - oa0), fbytes = (uint32_t)(fa1 - fa0);
+      const char *src = nullptr;
+      uint32_t dst = 0, bytes = 0;
+      int64_t stride2 = 0;
+      if (lane < 2 * ncp) {
+        const int row_k = lane / ncp, piece = lane % ncp;
+        if (piece == 0) {
+          src = reinterpret_cast<const char *>(args.orig) + (a * T + t) * H * rowb + oa0 + row_k * rowb;
+          dst = in_ring + row_k * geo.ob;
+          bytes = obytes;
+          stride2 = 2 * rowb;
+        } else {
+          const int j = PCA ? piece - 1 : g * k8GB + piece - 1;  // frame plane
+          src = reinterpret_cast<const char *>(args.frames) +
+                ((((a * args.G + j / 3) * T + t) * 3 + j % 3) * HW) * FSZ + fa0 + row_k * W * FSZ;
+          dst = in_ring + 2 * geo.ob + ((piece - 1) * 2 + row_k) * geo.fb;
+          bytes = fbytes;
+          stride2 = 2 * W * FSZ;
+        }
+      }
+      const uint32_t tx = obytes + (uint32_t)np * fbytes;
+      int st = 0;
+#pragma unroll 1
+      for (int p = 0; p < npairs; ++p) {
+        if (p >= ns) nbar_sync(k8BarStage + st, 32 * (k8VW + 1));  // parked until the 16 vertical warps released it
+        const int rows = min(2, H32 - 2 * p);
+        if (lane == 0) mbar_arrive_tx8(full_in + 8 * st, (uint32_t)rows * tx);
+        __syncwarp();
+        if (lane < rows * ncp) bulk_g2s8(dst + (uint32_t)st * geo.stage, src, bytes, full_in + 8 * st);
+        src += stride2;
+        if (++st == ns) st = 0;
+      }
+    } else {
+      // ---------------------------------------------------------------- horizontal workers
+      // task k = (filtered pair k / 8, row (k / 4) % 2, band k % 4); worker h takes h, h + 11, ...
+      const int hlim = min(k8Out, W32 - kSsimTaps - (int)x0 + 1);  // valid output columns of the strip
+      const bool hv_any = 4 * lane < hlim;
+      constexpr uint32_t kVbPair = 2u * k8VbRow * 16u;
+      const uint32_t cst = s0 + geo.off_desc;
+      float hs4 = 0.f;
+      const int ntask = nfe * 2 * k8GB;
+#pragma unroll 1
+      for (int k = h; k < ntask; k += k8HWork) {
+        const int e = k >> 3, hsub = (k >> 2) & 1, bb = k & 3;
+        const int slot = e % k8Ring;
+        nbar_sync(k8BarFilled + slot, k8BarCount);
+        if (bb < nb && hv_any && 2 * e + hsub <= H32 - kSsimTaps) {
+          const float4 cc = lds8_f32x4(cst + 16u * (uint32_t)bb);
+          const uint32_t hv = vb + 16u * (uint32_t)(vb8_skew(bb) + lane) + (uint32_t)slot * kVbPair +
+                              (uint32_t)hsub * (k8VbRow * 16u);
+          float2 asd[4], aq[4];
+          // loads run kHPf columns ahead of the filter (the chain is otherwise bound
+          // by one shared-memory latency per column)
+          constexpr int kHPf = 3;
+          float4 pf[kHPf];
+#pragma unroll
+          for (int kk = 0; kk < kHPf; ++kk) pf[kk] = lds8_f32x4(hv + 16u * (uint32_t)((kk & 3) * 34 + (kk >> 2)));
+#pragma unroll
+          for (int kk = 0; kk < 14; ++kk) {
+            const float4 v = pf[kk % kHPf];
+            if (kk + kHPf < 14)
+              pf[kk % kHPf] = lds8_f32x4(hv + 16u * (uint32_t)(((kk + kHPf) & 3) * 34 + ((kk + kHPf) >> 2)));
+            const float2 vsd = make_float2(v.x, v.y), vq = make_float2(v.z, v.w);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int tp = kk - i;
+              if (tp < 0 || tp > 10) continue;
+              const float wt = gtap(tp < 5 ? 5 - tp : tp - 5);
+              if (tp == 0) {
+                asd[i] = __fmul2_rn(vsd, make_float2(wt, wt));
+                aq[i] = __fmul2_rn(vq, make_float2(wt, wt));
+              } else {
+                asd[i] = __ffma2_rn(vsd, make_float2(wt, wt), asd[i]);
+                aq[i] = __ffma2_rn(vq, make_float2(wt, wt), aq[i]);
+              }
+            }
+          }
+          float ts = 0.f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float s1 = ssim_px(asd[i].x, asd[i].y, aq[i].x, aq[i].y, cc.x, cc.y, cc.z);
+            ts += 4 * lane + i < hlim ? s1 : 0.f;
+          }
+          hs4 += ts;
+        }
+        if (e + k8Ring < nfe) nbar_arrive(k8BarDrained + slot, k8BarCount);
+#pragma unroll
+        for (int bq = 0; bq < k8GB; ++bq)
+          if (bb == bq) hsumb[bq] += (double)hs4;
+        hs4 = 0.f;
+      }
+    }
+    __syncthreads();  // the ring is idle
+#pragma unroll
+    for (int bq = 0; bq < k8GB; ++bq) red[k8VW * 32 + (h * 32 + lane) * k8GB + bq] = hsumb[bq];
+    __syncthreads();  // all partials written
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(k8RegsV));
+
+  // ------------------------------------------------------------------ vertical warps
+  const int b = lane & 3, cl = lane >> 2;
+  const int lc = 8 * w + cl;  // local input column
+  const int c = g * k8GB + b;
+  const bool bact = b < nb;
+  const int xv = (int)x0 + lc;
+  const bool own = bact && xv < W32 && (lc < k8Out || last_strip);
+  const float c0 = bact ? (float)args.peaks[a * C + c] : 1.f;
+
+  // decode constants
+  double dq_m = 0.0, dq_span = 0.0;
+  float base = 0.f;
+  if constexpr (MODE == K8_F64) {
+    if (bact) {
+      dq_m = args.qmins[a * C + c];
+      dq_span = __dsub_rn(args.qmaxs[a * C + c], dq_m);
+    }
+  }
+  if constexpr (PCA) {
+    // recon_c = mean_c + sum_j (min_j + q_j span_j / L) W[j][c]
+    //         = base_c + sum_j q_j coef_cj   (float32; |error| << one code step);
+    // the coefficients live in shared memory (table written before the first barrier)
+    double bd = inv.mean[bact ? c : 0];
+#pragma unroll
+    for (int j = 0; j < EP; ++j)
+      if ((EXACT || j < E) && bact) bd = __fma_rn(args.qmins[a * E + j], inv.W[j * kMaxC + c], bd);
+    base = (float)bd;
+  }
+  const uint32_t coef_b = opaque8(s0 + geo.off_coef + (uint32_t)(b * k8PcaMax * 4));
+
+  // per-lane shared-memory byte offsets inside a stage. Lanes of an absent
+  // band (b >= nb) read the neighbouring band's finite values, lanes past the
+  // frame edge read zeros: neither reaches a counted output, so only the
+  // squared error and the recon store are masked.
+  const uint32_t o_off = opaque8(in_ring + (uint32_t)((x0 * C * 4) & 15) + (uint32_t)(lc * C + min(c, C - 1)) * 4u);
+  const uint32_t f_off = opaque8(in_ring + 2u * geo.ob + (uint32_t)((PCA ? 0 : 2 * min(b, nb - 1)) * geo.fb) +
+                                 (uint32_t)((x0 * FSZ) & 15) + (uint32_t)(lc * FSZ));
+  const uint32_t ob = opaque8(geo.ob), fb = opaque8(geo.fb), stage_b = opaque8(geo.stage);
+  const uint32_t lut_b = opaque8(s0 + geo.off_lut + (uint32_t)(b * k8LutMax * 8));
+  const uint32_t bars = opaque8(s0);  // full_in at +8*stage, empty_in at +8*(NS+stage)
+  uint32_t qor = 0;
+  float sse_f = 0.f;
+  double sse = 0.0;
+  const bool wr = args.recon_out != nullptr && own;
+  float *wq = args.recon_out + (a * T + t) * HW * C + (int64_t)xv * C + c;
+  const int64_t rstride = W * C;  // recon row stride (floats)
+
+  Fir8 fir;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    fir.zsd[i] = make_float2(0.f, 0.f);
+    fir.zq[i] = make_float2(0.f, 0.f);
+  }
+
+  constexpr uint32_t kVbPair = 2u * k8VbRow * 16u;  // bytes of one ring slot (row pair)
+  const uint32_t vb_st = opaque8(vb + 16u * (uint32_t)(vb8_skew(b) + vb8_idx(lc)));
+
+  int in_st = 0;          // input ring stage of the next pair
+  uint32_t in_off = 0;    // its byte offset
+  uint32_t in_ph = 0;     // parity of its "copies landed" completion
+  int vs_slot = 0;        // ring slot of the next filtered pair
+  uint32_t vs_off = 0;    // its byte offset
+#pragma unroll 1
+  for (int p = 0; p < npairs; ++p) {
+    const int U = in_st;
+    const uint32_t st = in_off;
+    const bool rel = p + ns < npairs;  // the loader refills this stage: tell it when the reads are done
+    mbar_wait8(bars + 8 * U, in_ph);
+    in_off += stage_b;
+    if (++in_st == ns) {
+      in_st = 0;
+      in_off = 0;
+      in_ph ^= 1u;
+    }
+    // raw inputs of the pair: original values and codes
+    float2 om;
+    om.x = lds8_f32(st + o_off);
+    om.y = lds8_f32(st + ob + o_off);
+    float2 rv, df;
+    if constexpr (PCA) {
+      uint32_t q0[EPL], q1[EPL];
+#pragma unroll
+      for (int j = 0; j < EP; ++j)
+        if (EXACT || j < E) {
+          q0[j] = lds8_code<FSZ>(st + f_off + (uint32_t)(2 * j) * fb);
+          q1[j] = lds8_code<FSZ>(st + f_off + (uint32_t)(2 * j + 1) * fb);
+        }
+      if (rel) nbar_arrive(k8BarStage + U, 32 * (k8VW + 1));
+      // both rows at once: acc = base + sum_j q_j coef_j (packed FFMA2)
+      float2 acc = make_float2(base, base);
+#pragma unroll
+      for (int j = 0; j < EP; j += 2) {
+        const float2 cf = lds8_f32x2(coef_b + 4u * (uint32_t)j);
+        if (EXACT || j < E) {
+          qor |= q0[j] | q1[j];
+          acc = __ffma2_rn(make_float2((float)q0[j], (float)q1[j]), make_float2(cf.x, cf.x), acc);
+        }
+        if (j + 1 < EP && (EXACT || j + 1 < E)) {
+          qor |= q0[j + 1] | q1[j + 1];
+          acc = __ffma2_rn(make_float2((float)q0[j + 1], (float)q1[j + 1]), make_float2(cf.y, cf.y), acc);
+        }
+      }
+      rv = acc;
+      df = fsub2_8(om, rv);
+    } else {
+      const uint32_t q0 = lds8_code<FSZ>(st + f_off), q1 = lds8_code<FSZ>(st + f_off + fb);
+      qor |= q0 | q1;
+      if constexpr (MODE == K8_LUT) {
+        const float2 l0 = lds8_f32x2(lut_b + 8u * min(q0, (uint32_t)(k8LutMax - 1)));
+        const float2 l1 = lds8_f32x2(lut_b + 8u * min(q1, (uint32_t)(k8LutMax - 1)));
+        if (rel) nbar_arrive(k8BarStage + U, 32 * (k8VW + 1));
+        rv = make_float2(l0.x, l1.x);
+        df = fsub2_8(fsub2_8(om, rv), make_float2(l0.y, l1.y));
+      } else {
+        if (rel) nbar_arrive(k8BarStage + U, 32 * (k8VW + 1));
+        const double rm0 = dequantize_fast(q0, dq_m, dq_span, L, args.rL);
+        const double rm1 = dequantize_fast(q1, dq_m, dq_span, L, args.rL);
+        rv = make_float2((float)rm0, (float)rm1);
+        df = make_float2((float)__dsub_rn((double)om.x, rm0), (float)__dsub_rn((double)om.y, rm1));
+      }
+    }
+    const bool ok1 = 2 * p + 1 < H32;  // odd H: the last pair's second row does not exist
+    if (wr) {  // the four bands of a pixel sit in adjacent lanes: 16-byte runs per pixel
+      wq[0] = rv.x;
+      if (ok1) wq[rstride] = rv.y;
+    }
+    wq += 2 * rstride;
+    const float d0 = own ? df.x : 0.f, d1 = (own && ok1) ? df.y : 0.f;
+    sse_f = fmaf(d1, d1, fmaf(d0, d0, sse_f));
+    const float2 sv = __fadd2_rn(__fadd2_rn(om, rv), make_float2(-2.f * c0, -2.f * c0));
+    const float4 o0 = fir8_step(fir, make_float2(sv.x, df.x));
+    const float4 o1 = fir8_step(fir, make_float2(sv.y, df.y));
+    if (p >= 5) {  // column-filtered rows 2p-10, 2p-9 = pair p-5
+      if (p - 5 >= k8Ring) nbar_sync(k8BarDrained + vs_slot, k8BarCount);
+      const uint32_t d = vb_st + vs_off;
+      sts8_f32x4(d, o0);
+      sts8_f32x4(d + k8VbRow * 16u, o1);
+      nbar_arrive(k8BarFilled + vs_slot, k8BarCount);
+      vs_off += kVbPair;
+      if (++vs_slot == k8Ring) {
+        vs_slot = 0;
+        vs_off = 0;
+      }
+    }
+    if ((p & 3) == 3) {
+      sse += (double)sse_f;
+      sse_f = 0.f;
+    }
+  }
+  sse += (double)sse_f;
+  flag_warp(args.err, (qor & ~args.Li) != 0u, CV_FLAG_INT_RANGE);
+
+  // deterministic CTA reduction: per band, fixed order over warps and lanes
+  __syncthreads();  // the ring is idle
+  red[w * 32 + lane] = sse;
+  __syncthreads();  // all partials written
+  if (threadIdx.x < nb) {
+    const int bq = threadIdx.x;
+    double s1 = 0.0, s2 = 0.0;
+    for (int ww = 0; ww < k8VW; ++ww)
+      for (int l = bq; l < 32; l += 4) s1 += red[ww * 32 + l];
+    for (int i = 0; i < k8HW * 32; ++i) s2 += red[k8VW * 32 + i * k8GB + bq];
+    double *pp = args.part + ((a * T + t) * args.nstrips + strip) * 2 * C;
+    pp[g * k8GB + bq] = s1;
+    pp[C + g * k8GB + bq] = s2;
+  }
+}
+
+}  // namespace cvb

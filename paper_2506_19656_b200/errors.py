@@ -1,23 +1,30 @@
-"""Exception hierarchy of the drop-in, same names and nesting as the reference's
-``cubevid.errors`` (/root/reference/pkg/src/cubevid/errors.py:4-21), so callers
-catching ``ConfigurationError`` keep working."""
+"""Exception hierarchy of the drop-in.
 
+When the reference package is importable its own classes are re-exported, so
+``except cubevid.errors.ConfigurationError`` in existing callers catches what
+this path raises without any aliasing; otherwise the same names and nesting
+are defined here (/root/reference/pkg/src/cubevid/errors.py:4-21).
+"""
 
-class CubevidError(Exception):
-    """Base class for all errors raised by the B200 path."""
+try:  # the reference's own classes, when it is installed next to this package
+    from cubevid.errors import (CodecError, ConfigurationError, CorruptStreamError,  # noqa: F401
+                                CubevidError, ManifestError)
 
+    SHARED_WITH_REFERENCE = True
+except ImportError:
+    SHARED_WITH_REFERENCE = False
 
-class ConfigurationError(CubevidError):
-    """Invalid bit depth, range, shape or non-finite data (reference convention)."""
+    class CubevidError(Exception):
+        """Base class for all errors raised by the B200 path."""
 
+    class ConfigurationError(CubevidError):
+        """Invalid bit depth, range, shape or non-finite data (reference convention)."""
 
-class CodecError(CubevidError):
-    """Kept for interface parity; the codec itself is outside this path."""
+    class CodecError(CubevidError):
+        """The external encoder or decoder failed (raised by codec plug-ins)."""
 
+    class CorruptStreamError(CodecError):
+        """Frame buffers whose size is not a whole number of frames."""
 
-class CorruptStreamError(CodecError):
-    """Frame buffers whose size is not a whole number of frames."""
-
-
-class ManifestError(CubevidError):
-    """Kept for interface parity with the reference container layer."""
+    class ManifestError(CubevidError):
+        """A container directory is missing files or carries a bad manifest."""

@@ -24,7 +24,8 @@ import torch
 
 from . import _device as dev
 from . import _lib
-from .errors import ConfigurationError
+from .bridge import check_stream_bytes
+from .errors import ConfigurationError, CorruptStreamError
 from .metrics import SSIM_WINDOW, psnr_from_sse
 from .plan import pack_groups
 from .transform import (SUPPORTED_BIT_DEPTHS, PcaModel, QuantParams, band_stats,
@@ -399,7 +400,17 @@ def decode_eval(enc: Encoded, orig=None, frames: torch.Tensor | None = None, wan
         raise ConfigurationError(f"spatial dims {H}x{W} smaller than the {SSIM_WINDOW}-px SSIM window")
     fr = enc.frames if frames is None else frames
     if tuple(fr.shape) != tuple(enc.frames.shape):
-        raise ConfigurationError("decoded frames do not match the encoded layout")
+        # a decoder handed back a different byte count: per video it must be a whole
+        # number of HxWx3 frames (bridge.py:163-171), and as many frames as were encoded
+        if fr.dtype != enc.frames.dtype:
+            raise ConfigurationError(f"decoded frames are {fr.dtype}, the stream is {enc.frames.dtype}")
+        n_videos = B * len(enc.groups)
+        n_bytes = fr.numel() * fr.element_size()
+        per_video = n_bytes // n_videos if n_bytes % n_videos == 0 else n_bytes
+        got = check_stream_bytes(per_video, H, W, 3, enc.spec.bit_depth)
+        if n_bytes % n_videos != 0 or got != T:
+            raise CorruptStreamError(f"decoded {got} frames per video, the stream holds {T}")
+        fr = fr.contiguous().view(enc.frames.shape)
     d = o.device
     s = dev.stream_ptr(d)
     lib = _lib.load()

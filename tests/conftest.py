@@ -49,7 +49,8 @@ def variant_sel():
     """Select kernel variants (cv_set_variant) for one test; restores the defaults."""
     from paper_2506_19656_b200 import _lib
 
-    defaults = {"gram_tiles": 0, "gram_nt": 64, "proj_nopf": 0, "qp_px1": 0, "qp_runtime_c": 0}
+    defaults = {"gram_tiles": 0, "gram_nt": 64, "proj_nopf": 0, "qp_px1": 0, "qp_runtime_c": 0,
+                "eval_kernel": 0}
 
     def sel(variants: dict):
         for k, v in variants.items():

@@ -177,6 +177,46 @@ def main():
     g["stream_recon"] = rt.dequantize(sq, sp)
     g["stream_filled"] = sf
 
+    # ---- select_for_video (cube.py:249-305), MappingRule / plan_stream (plan.py:26-66, 131-139),
+    # CorruptStreamError (bridge.py:163-171); own generator so the arrays above never change
+    r2 = np.random.default_rng(2506_19656 + 1)
+    va = r2.random((6, 9, 130)).astype(np.float32)            # (time, y, x)
+    vb = r2.random((130, 6, 9)).astype(np.float32)            # (x, time, y)
+    vc = r2.random((9, 130, 6)).astype(np.float32)            # (y, x, time)
+    v4 = r2.integers(0, 60000, (5, 6, 7, 9)).astype(np.uint16)  # (band, time, x, y)
+    g["sel_a"], g["sel_b"], g["sel_c"], g["sel_4d"] = va, vb, vc, v4
+    dc = rcube.DataCube({"a": va, "b": vb, "c": vc, "v4": v4},
+                        {"a": ("time", "y", "x"), "b": ("x", "time", "y"), "c": ("y", "x", "time"),
+                         "v4": ("band", "time", "x2", "y2")})
+    g["sel_abc"] = rcube.select_for_video(dc, ["a", "b", "c"], ("time", "y", "x"))
+    g["sel_cb_yxt"] = rcube.select_for_video(dc, ["c", "b"], ("y", "x", "time"))
+    g["sel_4d_out"] = rcube.select_for_video(dc, "v4", ("time", "y2", "x2"))
+    for key, names, order in (("sel_axis3", ["a"], ("time", "y")), ("sel_dup", ["a", "a"], ("time", "y", "x")),
+                              ("sel_empty", [], ("time", "y", "x")), ("sel_missing", ["zz"], ("time", "y", "x")),
+                              ("sel_mix", ["a", "v4"], ("time", "y", "x")),
+                              ("sel_axes", ["a"], ("time", "y", "lon")),
+                              ("sel_4d_axes", ["v4"], ("time", "y", "x"))):
+        try:
+            rcube.select_for_video(dc, names, order)
+        except ConfigurationError as e:
+            errors[key] = str(e)
+    for key, kw in (("rule_noname", dict(stream_name="", input_vars=("a",), axis_order=("t", "y", "x"))),
+                    ("rule_novars", dict(stream_name="s", input_vars=(), axis_order=("t", "y", "x"))),
+                    ("rule_axes", dict(stream_name="s", input_vars=("a",), axis_order=("t", "y"))),
+                    ("rule_npcs", dict(stream_name="s", input_vars=("a",), axis_order=("t", "y", "x"), n_pcs=-1)),
+                    ("rule_depth", dict(stream_name="s", input_vars=("a",), axis_order=("t", "y", "x"),
+                                        out_bit_depth=9))):
+        try:
+            rplan.MappingRule(**kw)
+        except ConfigurationError as e:
+            errors[key] = str(e)
+    rule = rplan.MappingRule("s", ("a", "b"), ("time", "y", "x"), n_pcs=4)
+    groups["rule_npcs4_of_7"] = [[gr.video_index, list(gr.members), gr.n_real] for gr in rplan.plan_stream(rule, 7)]
+    try:
+        rbridge._planar_bytes_to_frames(b"\x00" * 7, 4, 5, 3, 10)
+    except Exception as e:  # CorruptStreamError
+        errors["corrupt_stream"] = f"{type(e).__name__}: {e}"
+
     np.savez_compressed(OUT / "golden.npz", **g)
     (OUT / "golden_groups.json").write_text(json.dumps(groups))
     (OUT / "golden_errors.json").write_text(json.dumps(errors, indent=1))

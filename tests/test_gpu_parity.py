@@ -444,7 +444,10 @@ def test_gram_kernels_ragged(cuda, variant_sel, C, n_pix, variant):
     ((2, 16, 64, 12), 12, 9, False),     # PCA 12->9
     ((1, 21, 128, 8), 8, 5, False),      # 8-bit PCA planes, generic plane count
 ])
-def test_ssim_bulk_kernel_shapes(cuda, shape, bits, n_pcs, noisy):
+@pytest.mark.parametrize("kernel", [7, 8])
+def test_ssim_bulk_kernel_shapes(cuda, variant_sel, shape, bits, n_pcs, noisy, kernel):
+    """Both bulk-copy SSIM kernels (k_eval_ssim7 / k_eval_ssim8) in every decode mode."""
+    variant_sel({"eval_kernel": kernel})
     rng = np.random.default_rng(sum(shape) + bits)
     T, H, W, C = shape
     yy, xx = np.mgrid[0:H, 0:W]

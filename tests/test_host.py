@@ -125,3 +125,69 @@ def test_synth_small_shapes():
     assert e.shape == (2, 19, 36, 12) and float(e[..., 11].mean()) > 1e3 * float(e[..., 0].mean())
     s = synth.simple_s2(shape=(2, 32, 32, 12))
     assert s.shape == (2, 32, 32, 12)
+
+
+def test_mapping_rule_and_plan_stream(golden_errors, golden_groups):
+    ok = dict(stream_name="s", input_vars=("a",), axis_order=("t", "y", "x"))
+    for key, kw in (("rule_noname", dict(ok, stream_name="")), ("rule_novars", dict(ok, input_vars=())),
+                    ("rule_axes", dict(ok, axis_order=("t", "y"))), ("rule_npcs", dict(ok, n_pcs=-1)),
+                    ("rule_depth", dict(ok, out_bit_depth=9))):
+        with pytest.raises(ConfigurationError) as e:
+            P.MappingRule(**kw)
+        assert str(e.value) == golden_errors[key]
+    rule = P.MappingRule("s", "a", ("time", "y", "x"), n_pcs=4)
+    assert rule.input_vars == ("a",) and not rule.config_is_list
+    got = [[g.video_index, list(g.members), g.n_real] for g in P.plan_stream(rule, 7)]
+    assert got == golden_groups["rule_npcs4_of_7"]
+    assert len(P.plan_stream(P.MappingRule("s", "a", ("time", "y", "x")), 7)) == 3
+
+
+def test_select_for_video_validation(golden, golden_errors):
+    from paper_2506_19656_b200 import cube as Cb
+
+    dc = Cb.DataCube({"a": golden["sel_a"], "v4": golden["sel_4d"]},
+                     {"a": ("time", "y", "x"), "v4": ("band", "time", "x2", "y2")})
+    assert "a" in dc and dc.axis_length("x") == 130 and dc.variable_names() == ("a", "v4")
+    assert Cb.channel_axis_of(dc, "v4", ("time", "y2", "x2")) == "band"
+    for key, names, order in (("sel_axis3", ["a"], ("time", "y")), ("sel_dup", ["a", "a"], ("time", "y", "x")),
+                              ("sel_empty", [], ("time", "y", "x")), ("sel_missing", ["zz"], ("time", "y", "x")),
+                              ("sel_mix", ["a", "v4"], ("time", "y", "x")),
+                              ("sel_axes", ["a"], ("time", "y", "lon")),
+                              ("sel_4d_axes", ["v4"], ("time", "y", "x"))):
+        with pytest.raises(ConfigurationError) as e:
+            Cb.select_for_video(dc, names, order)
+        assert str(e.value) == golden_errors[key], key
+    with pytest.raises(ConfigurationError):
+        Cb.DataCube({"a": golden["sel_a"]}, {"a": ("t", "y")})
+    with pytest.raises(ConfigurationError):
+        Cb.DataCube({"a": golden["sel_a"], "b": golden["sel_b"]}, {"a": ("t", "y", "x"), "b": ("t", "y", "x")})
+
+
+def test_corrupt_stream_error(golden_errors):
+    from paper_2506_19656_b200 import CodecError, CorruptStreamError
+    from paper_2506_19656_b200.bridge import _planar_bytes_to_frames, check_stream_bytes
+
+    with pytest.raises(CorruptStreamError) as e:
+        _planar_bytes_to_frames(b"\x00" * 7, 4, 5, 3, 10)
+    assert f"CorruptStreamError: {e.value}" == golden_errors["corrupt_stream"]
+    assert issubclass(CorruptStreamError, CodecError)
+    assert check_stream_bytes(4 * 5 * 3 * 2 * 6, 4, 5, 3, 10) == 6
+    with pytest.raises(CorruptStreamError):
+        check_stream_bytes(10, 0, 5, 3, 8)
+
+
+def test_errors_are_the_reference_classes_when_importable():
+    """With cubevid on the path the drop-in raises the reference's own classes."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    ref = Path("/root/reference/pkg/src")
+    if not ref.exists():
+        pytest.skip("the reference tree only exists in the build container")
+    root = Path(__file__).resolve().parents[1]
+    code = ("import cubevid.errors as r, paper_2506_19656_b200.errors as e;"
+            "assert e.SHARED_WITH_REFERENCE and e.ConfigurationError is r.ConfigurationError "
+            "and e.CorruptStreamError is r.CorruptStreamError")
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root,
+                   env={"PYTHONPATH": f"{ref}:{root}", "PATH": "/usr/bin:/bin"})

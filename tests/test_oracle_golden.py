@@ -108,3 +108,20 @@ def test_stream_composition(golden):
     np.testing.assert_array_equal(enc["frames"], golden["stream_frames"])
     rec = O.decode_stream(enc["frames"], enc, golden["stream_in"].shape, 10)
     np.testing.assert_array_equal(rec, golden["stream_recon"])
+
+
+def test_select_for_video(golden):
+    v = {k: golden[f"sel_{k}"] for k in ("a", "b", "c")}
+    v["v4"] = golden["sel_4d"]
+    ax = {"a": ("time", "y", "x"), "b": ("x", "time", "y"), "c": ("y", "x", "time"),
+          "v4": ("band", "time", "x2", "y2")}
+    np.testing.assert_array_equal(O.select_for_video(v, ax, ["a", "b", "c"], ("time", "y", "x")), golden["sel_abc"])
+    np.testing.assert_array_equal(O.select_for_video(v, ax, ["c", "b"], ("y", "x", "time")), golden["sel_cb_yxt"])
+    out = O.select_for_video(v, ax, "v4", ("time", "y2", "x2"))
+    assert out.dtype == np.uint16
+    np.testing.assert_array_equal(out, golden["sel_4d_out"])
+    for names, order in ((["a"], ("time", "y")), (["a", "a"], ("time", "y", "x")), ([], ("time", "y", "x")),
+                         (["zz"], ("time", "y", "x")), (["a", "v4"], ("time", "y", "x")),
+                         (["a"], ("time", "y", "lon")), (["v4"], ("time", "y", "x"))):
+        with pytest.raises(O.OracleError):
+            O.select_for_video(v, ax, names, order)

@@ -1,3 +1,9 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_parity.py -m gpu -x -q -k "fullsize or variants or gram_kernels" > gpurun_out/t_a2.log 2>&1; echo rc=$? >> gpurun_out/t_a2.log
-bash tools/profile_cfg.sh c5 5 "k_eval_ssim7 k_gram_px k_pca_project_px k_quantize_planar" --t 96
+TAG=s8k
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo rc=$? >> gpurun_out/smoke_$TAG.log
+if grep -q "rc=0" gpurun_out/smoke_$TAG.log; then
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/t_$TAG.log 2>&1; echo rc=$? >> gpurun_out/t_$TAG.log
+for c in 5 2 3; do
+  timeout 200 python bench.py --config $c --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b${c}_$TAG.log 2>&1; echo rc=$? >> gpurun_out/b${c}_$TAG.log
+done
+fi
