@@ -61,6 +61,9 @@ int cv_set_variant(const char *name, int value) {
     if (value != 64 && value != 256) return cvb::fail(CV_ERR_ARG, "gram_nt must be 64 or 256, got %d", value);
     v.gram_nt = value;
   } else if (n == "proj_nopf") v.proj_nopf = value != 0;
+  else if (n == "proj12") v.proj12 = value != 0;
+  else if (n == "gram_checks") v.gram_checks = value != 0;
+  else if (n == "gram12") v.gram12 = value != 0;
   else if (n == "qp_px1") v.qp_px1 = value != 0;
   else if (n == "qp_runtime_c") v.qp_runtime_c = value != 0;
   else if (n == "eval_kernel") {

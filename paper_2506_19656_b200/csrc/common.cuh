@@ -23,6 +23,9 @@ struct Variants {
   int gram_tiles = 0;    // 1: tiled k_gram instead of the pixel-per-lane k_gram_px
   int gram_nt = 64;      // k_gram_px CTA size: 64 or 256
   int proj_nopf = 0;     // 1: no next-pixel prefetch in k_pca_project_px (C = 12)
+  int proj12 = 1;        // 0: k_pca_project_px instead of k_pca_project12 (float32, C = 12, K in {6, 9})
+  int gram12 = 1;        // 0: k_gram_px instead of k_gram12 (float32, C = 12)
+  int gram_checks = 0;   // 1: per-element finite tests in k_gram_px (else NaN / inf are read off the sums)
   int qp_px1 = 0;        // 1: one pixel per thread in k_quantize_planar
   int qp_runtime_c = 0;  // 1: runtime band count for the C = 12 PCA quantiser
   int eval_kernel = 0;   // SSIM kernel: 0 = by decode mode (PCA: k_eval_ssim8, else k_eval_ssim7), 7 / 8 = forced

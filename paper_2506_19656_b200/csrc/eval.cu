@@ -80,22 +80,26 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
         constexpr int fsz = RS == RS_FRAMES_U8 ? 1 : 2;
         const int ngrp = (a.C + k8GB - 1) / k8GB;
         dim3 g8((unsigned)(ssim8_strips(a.W) * ngrp), (unsigned)a.T, (unsigned)n);
-#define CV_S8(MODE, EP, EX)                                                                                \
+#define CV_S8(MODE, EP, EX, CQ)                                                                              \
   do {                                                                                                   \
     const Ssim8Geom g8m = ssim8_geom(a.C, MODE == K8_PCA ? a.E : k8GB, fsz, MODE == K8_LUT);              \
     if (g8m.ns < 2) return fail(CV_ERR_UNSUPPORTED, "cv_eval: %d channels do not fit the SSIM kernel's rings", a.C); \
     const size_t sm = (size_t)g8m.total;                                                                 \
-    cudaFuncSetAttribute(k_eval_ssim8<RS, MODE, EP, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
-    k_eval_ssim8<RS, MODE, EP, EX><<<g8, k8Threads, sm, st>>>(a, inv);                                   \
+    cudaFuncSetAttribute(k_eval_ssim8<RS, MODE, EP, EX, CQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    k_eval_ssim8<RS, MODE, EP, EX, CQ><<<g8, k8Threads, sm, st>>>(a, inv);                               \
   } while (0)
+        // codes of a full-range depth (8-bit in u8, 16-bit in u16) cannot exceed L: no range test
+        const bool full = a.Li == (fsz == 1 ? 0xFFu : 0xFFFFu);
         if (pca) {
-          if (a.E == 6) CV_S8(K8_PCA, 6, true);
-          else if (a.E == 9) CV_S8(K8_PCA, 9, true);
-          else CV_S8(K8_PCA, k8PcaMax, false);
+          if (a.E == 6 && full) CV_S8(K8_PCA, 6, true, false);
+          else if (a.E == 6) CV_S8(K8_PCA, 6, true, true);
+          else if (a.E == 9 && full) CV_S8(K8_PCA, 9, true, false);
+          else if (a.E == 9) CV_S8(K8_PCA, 9, true, true);
+          else CV_S8(K8_PCA, k8PcaMax, false, true);
         } else if (a.bit_depth <= 10) {
-          CV_S8(K8_LUT, 0, false);
+          CV_S8(K8_LUT, 0, false, true);
         } else {
-          CV_S8(K8_F64, 0, false);
+          CV_S8(K8_F64, 0, false, true);
         }
 #undef CV_S8
         return check_launch("cv_eval(ssim8)");
@@ -260,6 +264,7 @@ int cv_eval(const void *frames, int32_t fdtype, int32_t E, const double *qmins, 
   // aligned rows (original W*C*4 and frame W*b bytes), <= 12 PCA planes
   const int fsz = fdtype == CV_U8 ? 1 : 2;
   a.ssim7 = ssim && frames && odtype == CV_F32 && (W * C) % 4 == 0 && (W * fsz) % 16 == 0 &&
+            H * W * C < (int64_t)1 << 31 &&
             ((uintptr_t)orig % 16) == 0 && ((uintptr_t)frames % 16) == 0 && (!pca || E <= k7PcaMax);
   if (a.ssim7) a.nstrips = ssim7_strips(W);
   // streaming PSNR-only kernel: frames, f32/u16 original, no PCA, C in {4, 7},

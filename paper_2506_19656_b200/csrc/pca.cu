@@ -183,7 +183,7 @@ __device__ __forceinline__ void gram_cp_async16(void *dst, const void *src) {
                : "memory");
 }
 
-template <int H, bool EXACT>
+template <int H, bool EXACT, bool CHK>
 __device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px, int C_, const float (&sh)[kGpxC],
                                                    double (&acc)[kGpxHalf], double (&bsum)[kGpxC / 2],
                                                    float (&mn)[kGpxC / 2], float (&mx)[kGpxC / 2], bool &isn,
@@ -204,15 +204,17 @@ __device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px,
 #pragma unroll
   for (int c = 0; c < kGpxC; ++c) {
     const double dd = __dsub_rn((double)x[c], (double)sh[c]);
-    d[c] = isfinite(dd) ? dd : 0.0;
+    d[c] = (!CHK || isfinite(dd)) ? dd : 0.0;
   }
 #pragma unroll
   for (int j = 0; j < kGpxC / 2; ++j) {
     const int c = H * (kGpxC / 2) + j;
     if (c < C) {
       const float v = x[c];
-      isn |= isnan(v);
-      nonfinite |= isinf(v);
+      if (CHK) {
+        isn |= isnan(v);
+        nonfinite |= isinf(v);
+      }
       mn[j] = fminf(mn[j], v);
       mx[j] = fmaxf(mx[j], v);
       bsum[j] = __dadd_rn(bsum[j], d[c]);
@@ -226,7 +228,12 @@ __device__ __forceinline__ void gram_px_accumulate(const float *__restrict__ px,
       if (k >= H * kGpxHalf && k < (H + 1) * kGpxHalf) acc[k - H * kGpxHalf] = __fma_rn(d[i], d[j], acc[k - H * kGpxHalf]);
 }
 
-template <int NT>
+// CHK = false (default): no per-element finite tests. A NaN anywhere makes the
+// products / sums of its band NaN and an infinity surfaces in the band's
+// min / max, so both flags are read off the per-thread results once at the end;
+// the sums of such a cube are not finite, and every caller discards them (fill
+// first, or raise).
+template <int NT, bool CHK>
 __global__ void __launch_bounds__(NT, NT <= 64 ? 5 : 1)
 k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restrict__ partials,
           StatsEntry *__restrict__ stats, uint32_t *err) {
@@ -283,16 +290,28 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
       const int pp = p + (NT / 2) * r;
       if ((b + it * G) * kGpxP + pp < n_pix) {
         if (C == kGpxC) {
-          if (H == 0) gram_px_accumulate<0, true>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
-          else gram_px_accumulate<1, true>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+          if (H == 0) gram_px_accumulate<0, true, CHK>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+          else gram_px_accumulate<1, true, CHK>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
         } else {
-          if (H == 0) gram_px_accumulate<0, false>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
-          else gram_px_accumulate<1, false>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+          if (H == 0) gram_px_accumulate<0, false, CHK>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
+          else gram_px_accumulate<1, false, CHK>(st + pp * C, C, sh, acc, bsum, mn, mx, isn, nonfinite);
         }
       }
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (!CHK) {
+#pragma unroll
+    for (int k = 0; k < kGpxHalf; ++k) isn |= isnan(acc[k]);
+#pragma unroll
+    for (int j = 0; j < kGpxC / 2; ++j) {
+      isn |= isnan(bsum[j]);
+      nonfinite |= isinf(mn[j]) && mn[j] <= mx[j];
+      nonfinite |= isinf(mx[j]) && mn[j] <= mx[j];
+    }
+#pragma unroll
+    for (int c = 0; c < kGpxC; ++c) isn |= isnan(sh[c]);
+  }
   flag_warp(err, nonfinite, CV_FLAG_NONFINITE);
   flag_warp(err, isn, CV_FLAG_NAN);
 
@@ -340,6 +359,204 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
       }
     } else if (idx - kGpxNP < C) {
       part[idx - kGpxNP] = s;
+    }
+  }
+}
+
+// Float32 cubes with exactly 12 bands: convert once, multiply from shared
+// float64 tiles. k_gram_px converts and shifts every pixel twice (once per
+// warp parity: 42 F2F + 28 DADD per pixel, XU pipe 43 % busy, 0.7 eligible
+// warps per scheduler at 162 registers). Here a CTA has two roles:
+//   * 3 converter warps (96 threads): thread i owns the 16-byte vectors
+//     i + 96 k of a 128-pixel chunk (always the same four bands 4 (i % 3) ..),
+//     copied with cp.async into a private 4-stage ring (only the copying
+//     thread reads them back: no CTA barrier), converts them to shifted float64
+//     once, keeps the band sums / min / max, and writes the pixel-major float64
+//     tile (stride 14 doubles: conflict-free 16-byte reads);
+//   * 4 product warps = 2 pairs x parity: a pair takes 64 pixels of the tile
+//     (two per lane), each parity half of the 78 products in registers.
+// Tiles are double-buffered and handed over with named barriers (arrive / sync).
+// Same shifted sums as k_gram_px (shift = first pixel), fixed-order reductions.
+constexpr int kG12C = 12;
+constexpr int kG12Conv = 96;                 // converter threads
+constexpr int kG12Prod = 128;                // product threads
+constexpr int kG12Threads = kG12Conv + kG12Prod;
+constexpr int kG12K = 4;                     // 16-byte vectors per converter thread per chunk
+constexpr int kG12Px = kG12Conv * kG12K / 3; // 128 pixels per chunk
+constexpr int kG12Stages = 4;
+constexpr int kG12PxStride = 14;             // doubles per pixel in the tile
+constexpr int kG12Ring = kG12Stages * kG12Conv * kG12K * 16;         // bytes
+constexpr int kG12Tile = kG12Px * kG12PxStride * 8;                  // bytes
+constexpr int kG12Smem = kG12Ring + 2 * kG12Tile;
+constexpr int kG12BarFull = 1, kG12BarEmpty = 3;
+
+__device__ __forceinline__ void g12_bar_sync(int id) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(kG12Threads) : "memory");
+}
+__device__ __forceinline__ void g12_bar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "n"(kG12Threads) : "memory");
+}
+
+template <int H>
+__device__ __forceinline__ void g12_products(const double *__restrict__ px, double (&acc)[kGpxHalf]) {
+  double d[kG12C];
+#pragma unroll
+  for (int q = 0; q < kG12C / 2; ++q) {
+    const double2 v = *reinterpret_cast<const double2 *>(px + 2 * q);
+    d[2 * q] = v.x;
+    d[2 * q + 1] = v.y;
+  }
+  int k = 0;
+#pragma unroll
+  for (int i = 0; i < kG12C; ++i)
+#pragma unroll
+    for (int j = i; j < kG12C; ++j, ++k)
+      if (k >= H * kGpxHalf && k < (H + 1) * kGpxHalf) acc[k - H * kGpxHalf] = __fma_rn(d[i], d[j], acc[k - H * kGpxHalf]);
+}
+
+__global__ void __launch_bounds__(kG12Threads, 2)
+k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ partials,
+         StatsEntry *__restrict__ stats, uint32_t *err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float4 *ring = reinterpret_cast<float4 *>(smem);
+  double *tiles = reinterpret_cast<double *>(smem + kG12Ring);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nvec = n_pix * 3;  // 16-byte vectors in the cube
+  const int64_t nchunks = (n_pix + kG12Px - 1) / kG12Px;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t nit = b < nchunks ? (nchunks - b + G - 1) / G : 0;
+  bool isn = false, nonfinite = false;
+  constexpr int RS = kGpxNP + kG12C;
+  double *red = reinterpret_cast<double *>(smem);  // end of kernel: [2 pairs][RS] + converter stats
+
+  if (warp < 3) {
+    // ------------------------------------------------------------ converters
+    const int i = tid, r = i % 3;
+    double shd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) shd[j] = (double)ldg(src + 4 * r + j);
+    float mn[4], mx[4];
+    double bs[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mn[j] = INFINITY, mx[j] = -INFINITY, bs[j] = 0.0;
+    auto issue = [&](int64_t it) {
+      if (it < nit) {
+        const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
+        float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
+#pragma unroll
+        for (int k = 0; k < kG12K; ++k)
+          if (v0 + kG12Conv * k < nvec) gram_cp_async16(st + kG12Conv * k, reinterpret_cast<const float4 *>(src) + v0 + kG12Conv * k);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < kG12Stages - 1; ++s0) issue(s0);
+    for (int64_t it = 0; it < nit; ++it) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kG12Stages - 2) : "memory");
+      issue(it + kG12Stages - 1);  // refills the stage this thread read one iteration ago
+      const int bf = (int)(it & 1);
+      if (it >= 2) g12_bar_sync(kG12BarEmpty + bf);
+      const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
+      const float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
+      double *tile = tiles + (size_t)bf * (kG12Px * kG12PxStride);
+#pragma unroll
+      for (int k = 0; k < kG12K; ++k) {
+        const int vl = i + kG12Conv * k;       // vector inside the chunk: pixel vl / 3, bands 4 r ..
+        double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
+        double d[4] = {0.0, 0.0, 0.0, 0.0};
+        if (v0 + kG12Conv * k < nvec) {
+          const float4 x = st[kG12Conv * k];
+          const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            mn[j] = fminf(mn[j], xv[j]);
+            mx[j] = fmaxf(mx[j], xv[j]);
+            d[j] = __dsub_rn((double)xv[j], shd[j]);
+            bs[j] = __dadd_rn(bs[j], d[j]);
+          }
+        }
+        *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
+        *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
+      }
+      g12_bar_arrive(kG12BarFull + bf);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      isn |= isnan(bs[j]) || isnan(shd[j]);
+      nonfinite |= mn[j] <= mx[j] && (isinf(mn[j]) || isinf(mx[j]));
+    }
+    flag_warp(err, nonfinite, CV_FLAG_NONFINITE);
+    flag_warp(err, isn, CV_FLAG_NAN);
+    __syncthreads();  // every tile / ring read is done: the shared memory becomes the reduction buffer
+    // converter stats: [96][4] sums, mins, maxs behind the product partials
+    double *cs = red + 2 * RS;
+    float *cf = reinterpret_cast<float *>(cs + kG12Conv * 4);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      cs[i * 4 + j] = bs[j];
+      cf[i * 8 + j] = mn[j];
+      cf[i * 8 + 4 + j] = mx[j];
+    }
+    __syncthreads();
+  } else {
+    // ------------------------------------------------------------ product warps
+    const int pw = warp - 3, H = pw & 1, pair = pw >> 1;
+    double acc[kGpxHalf];
+#pragma unroll
+    for (int k = 0; k < kGpxHalf; ++k) acc[k] = 0.0;
+    for (int64_t it = 0; it < nit; ++it) {
+      const int bf = (int)(it & 1);
+      g12_bar_sync(kG12BarFull + bf);
+      const double *tile = tiles + (size_t)bf * (kG12Px * kG12PxStride) + (size_t)(64 * pair + lane) * kG12PxStride;
+      if (H == 0) {
+        g12_products<0>(tile, acc);
+        g12_products<0>(tile + 32 * kG12PxStride, acc);
+      } else {
+        g12_products<1>(tile, acc);
+        g12_products<1>(tile + 32 * kG12PxStride, acc);
+      }
+      if (it + 2 < nit) g12_bar_arrive(kG12BarEmpty + bf);
+    }
+#pragma unroll
+    for (int k = 0; k < kGpxHalf; ++k) isn |= isnan(acc[k]);
+    flag_warp(err, isn, CV_FLAG_NAN);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < kGpxHalf; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < kGpxHalf; ++k) red[pair * RS + H * kGpxHalf + k] = acc[k];
+    __syncthreads();
+  }
+  // fixed-order CTA reduction (all threads)
+  double *part = partials + (size_t)b * (kG12C + kG12C * kG12C);
+  const double *cs = red + 2 * RS;
+  const float *cf = reinterpret_cast<const float *>(cs + kG12Conv * 4);
+  for (int idx = tid; idx < RS; idx += kG12Threads) {
+    if (idx < kGpxNP) {
+      const double s2 = red[idx] + red[RS + idx];
+      int i2 = 0, rem = idx;
+      while (rem >= kG12C - i2) rem -= kG12C - i2, ++i2;
+      const int j2 = i2 + rem;
+      part[kG12C + i2 * kG12C + j2] = s2;
+      part[kG12C + j2 * kG12C + i2] = s2;
+    } else {
+      const int c = idx - kGpxNP, r = c / 4, j = c % 4;
+      double s1 = 0.0;
+      float lo = INFINITY, hi = -INFINITY;
+      for (int t = r; t < kG12Conv; t += 3) {
+        s1 += cs[t * 4 + j];
+        lo = fminf(lo, cf[t * 8 + j]);
+        hi = fmaxf(hi, cf[t * 8 + 4 + j]);
+      }
+      part[c] = s1;
+      if (stats && lo <= hi) {
+        atomicMin(&stats[c].min_key, dkey((double)lo));
+        atomicMax(&stats[c].max_key, dkey((double)hi));
+      }
     }
   }
 }
@@ -562,6 +779,113 @@ k_pca_project_px(const TIn *__restrict__ src, int64_t n_pix, TO *__restrict__ ou
   }
 }
 
+// Projection of float32 cubes with exactly 12 bands (ERA5 / SimpleS2), K = KE
+// components. The weights sit in shared memory as float64 [KE][12] and are read
+// with one broadcast LDS.64 per weight that serves TWO pixels of the thread
+// (passed by value they end up in uniform registers, which spill at 72
+// weights: the k_pca_project_px capture shows R2UR / MOV.SPILL / STL traffic at
+// 36 thread-instructions per element against 6 DFMA). The next iteration's six
+// 16-byte loads are in flight during the projection. Bit-identical to
+// project_one (same fma order). A non-finite input makes every component
+// non-finite (NaN / inf propagate through the fma chain, also past zero
+// weights), so one check on the first component replaces the per-band tests.
+__device__ __forceinline__ double lds_f64_volatile(uint32_t a) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+  return v;
+}
+
+constexpr int kP12Threads = 256;
+
+template <typename TO, int KE>
+__global__ void __launch_bounds__(kP12Threads, 2)
+k_pca_project12(const float *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
+                StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err) {
+  constexpr int C = 12;
+  __shared__ double wsm[KE * C];
+  __shared__ double msm[C];
+  const int64_t a = blockIdx.y;
+  const float *cube = src + a * n_pix * C;
+  for (int i = threadIdx.x; i < KE * C; i += kP12Threads) wsm[i] = pca.W[(i / C) * kMaxC + i % C];
+  if (threadIdx.x < C) msm[threadIdx.x] = pca.mean[threadIdx.x];
+  __syncthreads();
+  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(wsm);
+  const uint32_t mbase = (uint32_t)__cvta_generic_to_shared(msm);
+  double mn[KE], mx[KE];
+#pragma unroll
+  for (int j = 0; j < KE; ++j) {
+    mn[j] = INFINITY;
+    mx[j] = -INFINITY;
+  }
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * (2 * kP12Threads);
+  auto load = [&](int64_t pix, float4 (&q)[3]) {
+#pragma unroll
+    for (int c4 = 0; c4 < 3; ++c4)
+      q[c4] = pix < n_pix ? __ldg(reinterpret_cast<const float4 *>(cube + pix * C) + c4)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float4 n0[3], n1[3];
+  int64_t pix = (int64_t)blockIdx.x * (2 * kP12Threads) + threadIdx.x;
+  load(pix, n0);
+  load(pix + kP12Threads, n1);
+  for (; pix < n_pix; pix += stride) {
+    double d0[C], d1[C];
+#pragma unroll
+    for (int c4 = 0; c4 < 3; ++c4) {
+      const double m0 = lds_f64_volatile(mbase + 8u * (4 * c4)), m1 = lds_f64_volatile(mbase + 8u * (4 * c4 + 1));
+      const double m2 = lds_f64_volatile(mbase + 8u * (4 * c4 + 2)), m3 = lds_f64_volatile(mbase + 8u * (4 * c4 + 3));
+      d0[4 * c4] = __dsub_rn((double)n0[c4].x, m0);
+      d0[4 * c4 + 1] = __dsub_rn((double)n0[c4].y, m1);
+      d0[4 * c4 + 2] = __dsub_rn((double)n0[c4].z, m2);
+      d0[4 * c4 + 3] = __dsub_rn((double)n0[c4].w, m3);
+      d1[4 * c4] = __dsub_rn((double)n1[c4].x, m0);
+      d1[4 * c4 + 1] = __dsub_rn((double)n1[c4].y, m1);
+      d1[4 * c4 + 2] = __dsub_rn((double)n1[c4].z, m2);
+      d1[4 * c4 + 3] = __dsub_rn((double)n1[c4].w, m3);
+    }
+    const bool v1 = pix + kP12Threads < n_pix;
+    load(pix + stride, n0);
+    load(pix + stride + kP12Threads, n1);
+#pragma unroll
+    for (int j = 0; j < KE; ++j) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double w = lds_f64_volatile(wbase + 8u * (uint32_t)(j * C + c));
+        a0 = __fma_rn(d0[c], w, a0);
+        a1 = __fma_rn(d1[c], w, a1);
+      }
+      if (j == 0) bad |= !isfinite(a0) || (v1 && !isfinite(a1));
+      mn[j] = fmin(mn[j], a0);
+      mx[j] = fmax(mx[j], a0);
+      if (v1) {
+        mn[j] = fmin(mn[j], a1);
+        mx[j] = fmax(mx[j], a1);
+      }
+      if (out) {
+        out[(a * n_pix + pix) * KE + j] = (TO)a0;
+        if (v1) out[(a * n_pix + pix + kP12Threads) * KE + j] = (TO)a1;
+      }
+    }
+  }
+  flag_warp(err, bad, CV_FLAG_NONFINITE);
+  if (stats) {
+#pragma unroll
+    for (int j = 0; j < KE; ++j) {
+      double a_mn = mn[j], a_mx = mx[j];
+      for (int o = 16; o > 0; o >>= 1) {
+        a_mn = fmin(a_mn, __shfl_xor_sync(0xffffffffu, a_mn, o));
+        a_mx = fmax(a_mx, __shfl_xor_sync(0xffffffffu, a_mx, o));
+      }
+      if ((threadIdx.x & 31) == 0 && a_mn <= a_mx) {
+        atomicMin(&stats[a * KE + j].min_key, dkey(a_mn));
+        atomicMax(&stats[a * KE + j].max_key, dkey(a_mx));
+      }
+    }
+  }
+}
+
 // Inverse projection: one thread per pixel.
 template <typename TIn, typename TO>
 __global__ void __launch_bounds__(256)
@@ -609,6 +933,19 @@ template <typename TIn>
 static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *out, void *stats,
                        uint32_t *err, cudaStream_t st) {
   if constexpr (std::is_same<TIn, float>::value) {
+    if (C == kG12C && ((uintptr_t)src & 15) == 0 && !g_variants.gram_tiles && g_variants.gram12) {
+      int64_t nblk = (n_pix + kG12Px - 1) / kG12Px;
+      if (nblk > 2 * (int64_t)num_sms()) nblk = 2 * (int64_t)num_sms();
+      const int64_t cap = gram_blocks(n_pix, C);  // the workspace holds this many partials
+      if (nblk > cap) nblk = cap;
+      cudaFuncSetAttribute(k_gram12, cudaFuncAttributeMaxDynamicSharedMemorySize, kG12Smem);
+      k_gram12<<<(unsigned)nblk, kG12Threads, kG12Smem, st>>>((const float *)src, n_pix, (double *)ws, (StatsEntry *)stats, err);
+      int s = check_launch("cv_pca_gram(12)");
+      if (s != CV_OK) return s;
+      const int stride = C + C * C;
+      k_reduce_partials<<<(stride + 7) / 8, 256, 0, st>>>((const double *)ws, (int)nblk, stride, out);
+      return check_launch("cv_pca_gram(reduce)");
+    }
     if (C <= kGpxC && ((uintptr_t)src & 15) == 0 && !g_variants.gram_tiles) {
       int nblk = gram_blocks(n_pix, C);
       if (nblk > num_sms()) nblk = num_sms();
@@ -617,7 +954,8 @@ static int launch_gram(const void *src, int64_t n_pix, int C, void *ws, double *
       size_t sm = (size_t)kGpxS * NT * C * sizeof(float);
       const size_t smr = (size_t)(NT / 64) * (kGpxNP + kGpxC) * sizeof(double);
       if (smr > sm) sm = smr;
-      auto kern = NT == 64 ? k_gram_px<64> : k_gram_px<256>;
+      auto kern = g_variants.gram_checks ? (NT == 64 ? k_gram_px<64, true> : k_gram_px<256, true>)
+                                         : (NT == 64 ? k_gram_px<64, false> : k_gram_px<256, false>);
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       kern<<<nblk, NT == 64 ? 64 : 256, sm, st>>>((const float *)src, n_pix, C, (double *)ws, (StatsEntry *)stats, err);
       int s = check_launch("cv_pca_gram(px)");
@@ -659,6 +997,23 @@ static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const
 #define CV_PX(KB, CM) \
   k_pca_project_px<TIn, TO, KB, CM, PPT><<<grid, NT, 0, st>>>((const TIn *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err)
     const bool al = ((uintptr_t)src & 15) == 0;
+    if constexpr (std::is_same<TIn, float>::value) {
+      if (p.C == 12 && al && g_variants.proj12 && (p.K == 6 || p.K == 9)) {
+        // shared-memory weights, two pixels per thread, two CTAs per SM
+        int64_t nb2 = (n_pix + 2 * kP12Threads - 1) / (2 * kP12Threads);
+        // exactly two resident CTAs per SM in total: one CTA more would run alone after the
+        // first wave (the i2 capture showed fp64-pipe max 67 % vs avg 45 % over the SMs)
+        int64_t cap2 = 2 * (int64_t)num_sms() / (n_cubes > 0 ? n_cubes : 1);
+        if (cap2 < 1) cap2 = 1;
+        if (nb2 > cap2) nb2 = cap2;
+        dim3 grid2((unsigned)(nb2 < 1 ? 1 : nb2), (unsigned)n_cubes);
+        if (p.K == 6)
+          k_pca_project12<TO, 6><<<grid2, kP12Threads, 0, st>>>((const float *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+        else
+          k_pca_project12<TO, 9><<<grid2, kP12Threads, 0, st>>>((const float *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+        return check_launch("cv_pca_project(12)");
+      }
+    }
     if (p.C == 12 && al) {  // e.g. ERA5 / SimpleS2: exact-width register arrays, 16-byte loads,
                             // one pixel per thread and two CTAs per SM
       int64_t nb1 = (n_pix + NT - 1) / NT;

@@ -385,7 +385,8 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
   const int P = px2 ? 2 * NT : NT;
   const int NE = P * args.C;
   const int SP = (NE + VE - 1) / VE * VE;
-  const size_t sm = (size_t)kQStages * SP * sizeof(TIn) + kMaxC * (sizeof(QBand) + sizeof(QBand32));
+  const size_t sm = (size_t)kQStages * SP * sizeof(TIn) + kMaxC * (sizeof(QBand) + sizeof(QBand32)) +
+                    (PCA ? kQP12Tab : 0);
   dim3 grid((unsigned)((args.HW + P - 1) / P), (unsigned)cv_num_segments(args.T, args.seg_len),
             (unsigned)n_cubes);
   const int mv = (P / NT * args.C + VE - 1) / VE;  // vectors per thread per step
@@ -395,7 +396,7 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
   } while (0)
-  if (px2 && PCA && args.C == 12 && mv <= 8 && mv > 4 && !g_variants.qp_runtime_c) {
+  if (px2 && PCA && args.C == 12 && mv <= 8 && mv > 4 && !g_variants.qp_runtime_c && !args.clamp) {
     auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, 8, true, 12>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);

@@ -37,6 +37,35 @@ __device__ __forceinline__ void cp_async_wait_q() {
 // stores both samples of a plane with one 32-bit (u16) / 16-bit (u8) store.
 constexpr int kQRegC = 8;
 constexpr int kQPcaC = 16;  // PCA register path: channels and components
+// C = 12 PCA path: float64 tables in shared memory behind the band constants:
+// weights [12][12], means [12], K = L / span [12]
+constexpr int kQP12 = 12;
+constexpr int kQP12Tab = (kQP12 * kQP12 + 2 * kQP12) * 8;
+
+__device__ __forceinline__ double lds_f64_q(uint32_t a) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+  return v;
+}
+
+// quantize (transform.py:98-105) of one float64 component. Fast path: one fma,
+// t = (v - m) K + 0.5 with K = RN(L / span); it differs from the reference's
+// RN(RN(RN(v - m) / span) L) + 0.5 by less than 4 L 2^-53 < 4e-11, so whenever
+// frac(t) is more than 2^-28 away from an integer both floors agree; otherwise
+// the reference's own operation order decides.
+// No clamping here (the launcher sends clamped streams to the generic kernel);
+// out-of-range / NaN values set `bad` (transform.py:92-97 raises).
+__device__ __forceinline__ uint32_t quantize_pc(double v, double m, double M, double s, double K, double L,
+                                                uint32_t &bad) {
+  if (!(v >= m && v <= M)) bad = 1u;
+  const double diff = __dsub_rn(v, m);
+  const double t = __fma_rn(diff, K, 0.5);
+  double q = floor(t);
+  const double fr = __dsub_rn(t, q);
+  const double eps = 3.725290298461914e-09;  // 2^-28
+  if (fr < eps || fr > 1.0 - eps) q = floor(__dadd_rn(__dmul_rn(__ddiv_rn(diff, s), L), 0.5));
+  return min((uint32_t)q, 65535u);  // a constant band has span 1 and v = m: t = 0.5, q = 0
+}
 
 template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false, int CX = 0>
 __global__ void __launch_bounds__(256)
@@ -65,6 +94,12 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   for (int j = tid; j < E; j += NT) {
     qtab[j] = make_qband(args.mins[a * E + j], args.maxs[a * E + j], args.bit_depth);
     qtab32[j] = make_qband32(qtab[j], args.clamp);
+  }
+  double *wsm = reinterpret_cast<double *>(qtab32 + kMaxC);  // [12][12] weights, [12] means, [12] K
+  if constexpr (PX2 && PCA && CX == kQP12) {
+    for (int i = tid; i < E * kQP12; i += NT) wsm[i] = pca.W[(i / kQP12) * kMaxC + i % kQP12];
+    if (tid < kQP12) wsm[kQP12 * kQP12 + tid] = pca.mean[tid];
+    for (int j = tid; j < E; j += NT) wsm[kQP12 * kQP12 + kQP12 + j] = __ddiv_rn(qtab[j].L, qtab[j].s);
   }
   __syncthreads();
 
@@ -139,7 +174,55 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
     // refill the stage consumed one step ago (every thread is past it now)
     if (t + kQStages - 1 < t1) issue(t + kQStages - 1);
     cp_async_commit_q();
-    if (PX2 && PCA && pvalid) {
+    if constexpr (PX2 && PCA && CX == kQP12) {
+      if (pvalid) {
+        // C = 12 pixel pair: weights / means / per-component constants through
+        // broadcast LDS.64 (one load serves both pixels; as kernel parameters the
+        // 72 weights overflow the uniform registers and spill), one fma per code
+        const TIn *px = st + p * kQP12;
+        TOut *op = obase + (t - t0) * 3 * HW;
+        using W2 = typename std::conditional<sizeof(TOut) == 1, uint16_t, uint32_t>::type;
+        const uint32_t wb = (uint32_t)__cvta_generic_to_shared(wsm);
+        const uint32_t qb = (uint32_t)__cvta_generic_to_shared(qtab);
+        double d0[kQP12], d1[kQP12];
+#pragma unroll
+        for (int c = 0; c < kQP12; ++c) {
+          const double mu = lds_f64_q(wb + 8u * (kQP12 * kQP12 + c));
+          d0[c] = __dsub_rn((double)px[c], mu);
+          d1[c] = __dsub_rn((double)px[kQP12 + c], mu);
+        }
+        uint32_t l0 = 0, l1 = 0, badi = 0;
+#pragma unroll
+        for (int pl = 0; pl < kQP12; ++pl) {
+          if (pl < 3 * args.G) {
+            uint32_t q0, q1;
+            if (pl < E) {
+              double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+              for (int c = 0; c < kQP12; ++c) {
+                const double w = lds_f64_q(wb + 8u * (uint32_t)(pl * kQP12 + c));
+                a0 = __fma_rn(d0[c], w, a0);
+                a1 = __fma_rn(d1[c], w, a1);
+              }
+              const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
+              const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8), bs = lds_f64_q(bq + 16), bL = lds_f64_q(bq + 32);
+              const double bK = lds_f64_q(wb + 8u * (uint32_t)(kQP12 * kQP12 + kQP12 + pl));
+              q0 = quantize_pc(a0, bm, bM, bs, bK, bL, badi);
+              q1 = quantize_pc(a1, bm, bM, bs, bK, bL, badi);
+              l0 = q0;
+              l1 = q1;
+            } else {
+              const bool rep = args.pad_mode == CV_PAD_REPEAT;
+              q0 = rep ? l0 : 0u;
+              q1 = rep ? l1 : 0u;
+            }
+            *reinterpret_cast<W2 *>(op) = (W2)(q0 | (q1 << (8 * sizeof(TOut))));
+            op += (pl % 3 == 2) ? gjump : HW;
+          }
+        }
+        bad |= badi != 0u;
+      }
+    } else if (PX2 && PCA && pvalid) {
       // PCA pixel pair (p, p+1): both projections in registers (two independent
       // float64 chains), one 32-bit / 16-bit store per component plane
       const TIn *px = st + p * C;

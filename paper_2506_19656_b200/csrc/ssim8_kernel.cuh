@@ -180,34 +180,46 @@ __device__ __forceinline__ uint32_t opaque8(uint32_t x) {
 // a - b on packed pairs (one rounding: b * -1 + a)
 __device__ __forceinline__ float2 fsub2_8(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
 
-// transposed-form 11-tap FIR on packed pairs: zsd = (s, d), zq = (s^2, d^2);
-// z[k] holds the partial sums of the output row completed k rows from now.
+// Transposed-form 11-tap FIR on packed pairs, updated IN PLACE: zsd = (s, d),
+// zq = (s^2, d^2). The output row born at step i lives in slot i % 10 for its
+// ten following steps; step S (= row index mod 10, a compile-time constant of
+// the 5-pair unrolled loop) completes and restarts slot S and adds the row to
+// the nine others with the weight of their age. Every FFMA2 has its
+// accumulator as destination: the shifting form (z[k-1] = p w + z[k]) made the
+// compiler rotate the 40 state registers with ~15 MOV / IMAD.MOV per row.
 struct Fir8 {
   float2 zsd[10], zq[10];
 };
 
+template <int S>
 __device__ __forceinline__ float4 fir8_step(Fir8 &f, float2 p) {
   const float2 q = __fmul2_rn(p, p);
   const float w0 = gtap(5);
-  const float2 osd = __ffma2_rn(p, make_float2(w0, w0), f.zsd[0]);
-  const float2 oq = __ffma2_rn(q, make_float2(w0, w0), f.zq[0]);
+  const float2 osd = __ffma2_rn(p, make_float2(w0, w0), f.zsd[S]);
+  const float2 oq = __ffma2_rn(q, make_float2(w0, w0), f.zq[S]);
+  f.zsd[S] = __fmul2_rn(p, make_float2(w0, w0));
+  f.zq[S] = __fmul2_rn(q, make_float2(w0, w0));
 #pragma unroll
-  for (int k = 1; k < 10; ++k) {
-    const float wt = gtap(k - 5 < 0 ? 5 - k : k - 5);
-    f.zsd[k - 1] = __ffma2_rn(p, make_float2(wt, wt), f.zsd[k]);
-    f.zq[k - 1] = __ffma2_rn(q, make_float2(wt, wt), f.zq[k]);
+  for (int age = 1; age < 10; ++age) {
+    const int j = (S - age + 10) % 10;
+    const float wt = gtap(age < 5 ? 5 - age : age - 5);
+    f.zsd[j] = __ffma2_rn(p, make_float2(wt, wt), f.zsd[j]);
+    f.zq[j] = __ffma2_rn(q, make_float2(wt, wt), f.zq[j]);
   }
-  f.zsd[9] = __fmul2_rn(p, make_float2(w0, w0));
-  f.zq[9] = __fmul2_rn(q, make_float2(w0, w0));
   return make_float4(osd.x, osd.y, oq.x, oq.y);
 }
+
+template <int U>
+struct PairIdx8 {
+  static constexpr int value = U;
+};
 
 __device__ __forceinline__ int vb8_skew(int b) { return b * k8VbBand + ((b & 1) | ((b & 2) << 1)); }  // {0,1,4,5} mod 8
 __device__ __forceinline__ int vb8_idx(int col) { return (col & 3) * 34 + (col >> 2); }
 
 // EP: PCA planes the loops are unrolled for; EXACT: E == EP (6 and 9), else
 // k8PcaMax with runtime guards; 0 without PCA.
-template <int RS, int MODE, int EP, bool EXACT>
+template <int RS, int MODE, int EP, bool EXACT, bool CHKQ = true>
 __global__ void __launch_bounds__(k8Threads, 1)
 k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   using R = typename RawT<RS>::type;
@@ -441,8 +453,10 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   float sse_f = 0.f;
   double sse = 0.0;
   const bool wr = args.recon_out != nullptr && own;
-  float *wq = args.recon_out + (a * T + t) * HW * C + (int64_t)xv * C + c;
-  const int64_t rstride = W * C;  // recon row stride (floats)
+  // recon stores: frame base (uniform) + 32-bit element offset inside the frame
+  float *const rbase = args.recon_out + (a * T + t) * HW * C;
+  uint32_t woff = (uint32_t)(xv * C + c);
+  const uint32_t rstride = (uint32_t)(W32 * C);  // recon row stride (floats); H W C < 2^31
 
   Fir8 fir;
 #pragma unroll
@@ -459,8 +473,11 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   uint32_t in_ph = 0;     // parity of its "copies landed" completion
   int vs_slot = 0;        // ring slot of the next filtered pair
   uint32_t vs_off = 0;    // its byte offset
-#pragma unroll 1
-  for (int p = 0; p < npairs; ++p) {
+  // one row pair; UU = pair index mod 5 (the FIR slots of its rows are 2 UU, 2 UU + 1)
+  // FIRST: pairs 0 .. 4, whose filtered rows do not exist yet (no ring writes)
+  auto pair_step = [&](auto uu, auto first, const int p) {
+    constexpr int UU = decltype(uu)::value;
+    constexpr bool FIRST = decltype(first)::value != 0;
     const int U = in_st;
     const uint32_t st = in_off;
     const bool rel = p + ns < npairs;  // the loader refills this stage: tell it when the reads are done
@@ -491,16 +508,15 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
       for (int j = 0; j < EP; j += 2) {
         const float2 cf = lds8_f32x2(coef_b + 4u * (uint32_t)j);
         if (EXACT || j < E) {
-          qor |= q0[j] | q1[j];
+          if (CHKQ) qor |= q0[j] | q1[j];
           acc = __ffma2_rn(make_float2((float)q0[j], (float)q1[j]), make_float2(cf.x, cf.x), acc);
         }
         if (j + 1 < EP && (EXACT || j + 1 < E)) {
-          qor |= q0[j + 1] | q1[j + 1];
+          if (CHKQ) qor |= q0[j + 1] | q1[j + 1];
           acc = __ffma2_rn(make_float2((float)q0[j + 1], (float)q1[j + 1]), make_float2(cf.y, cf.y), acc);
         }
       }
       rv = acc;
-      df = fsub2_8(om, rv);
     } else {
       const uint32_t q0 = lds8_code<FSZ>(st + f_off), q1 = lds8_code<FSZ>(st + f_off + fb);
       qor |= q0 | q1;
@@ -509,7 +525,7 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
         const float2 l1 = lds8_f32x2(lut_b + 8u * min(q1, (uint32_t)(k8LutMax - 1)));
         if (rel) nbar_arrive(k8BarStage + U, 32 * (k8VW + 1));
         rv = make_float2(l0.x, l1.x);
-        df = fsub2_8(fsub2_8(om, rv), make_float2(l0.y, l1.y));
+        df = make_float2(l0.y, l1.y);  // the low halves; subtracted from (o - hi) below
       } else {
         if (rel) nbar_arrive(k8BarStage + U, 32 * (k8VW + 1));
         const double rm0 = dequantize_fast(q0, dq_m, dq_span, L, args.rL);
@@ -520,16 +536,36 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
     }
     const bool ok1 = 2 * p + 1 < H32;  // odd H: the last pair's second row does not exist
     if (wr) {  // the four bands of a pixel sit in adjacent lanes: 16-byte runs per pixel
-      wq[0] = rv.x;
-      if (ok1) wq[rstride] = rv.y;
+      rbase[woff] = rv.x;
+      if (ok1) rbase[woff + rstride] = rv.y;
     }
-    wq += 2 * rstride;
+    woff += 2u * rstride;
+    // FIR inputs (s, d) = (x' + y', x - y) per row
+    float2 p0, p1;
+    if constexpr (PCA) {
+      // straight into (s, d) pairs from the row-packed decode, with broadcast
+      // operands: (o - 2 c0, o) + r (1, -1); no repacking moves
+      const float2 kpm = make_float2(1.f, -1.f), kc = make_float2(-2.f * c0, 0.f);
+      p0 = __ffma2_rn(make_float2(rv.x, rv.x), kpm, __fadd2_rn(make_float2(om.x, om.x), kc));
+      p1 = __ffma2_rn(make_float2(rv.y, rv.y), kpm, __fadd2_rn(make_float2(om.y, om.y), kc));
+      df = make_float2(p0.y, p1.y);
+    } else if constexpr (MODE == K8_LUT) {
+      // same pairs from the (hi, lo) table entries: d = (o - hi) - lo
+      const float2 kpm = make_float2(1.f, -1.f), kc = make_float2(-2.f * c0, 0.f);
+      p0 = __ffma2_rn(make_float2(rv.x, rv.x), kpm, __fadd2_rn(make_float2(om.x, om.x), kc));
+      p1 = __ffma2_rn(make_float2(rv.y, rv.y), kpm, __fadd2_rn(make_float2(om.y, om.y), kc));
+      p0.y = __fsub_rn(p0.y, df.x);
+      p1.y = __fsub_rn(p1.y, df.y);
+      df = make_float2(p0.y, p1.y);
+    } else {
+      p0 = make_float2(__fadd_rn(__fadd_rn(om.x, rv.x), -2.f * c0), df.x);
+      p1 = make_float2(__fadd_rn(__fadd_rn(om.y, rv.y), -2.f * c0), df.y);
+    }
     const float d0 = own ? df.x : 0.f, d1 = (own && ok1) ? df.y : 0.f;
     sse_f = fmaf(d1, d1, fmaf(d0, d0, sse_f));
-    const float2 sv = __fadd2_rn(__fadd2_rn(om, rv), make_float2(-2.f * c0, -2.f * c0));
-    const float4 o0 = fir8_step(fir, make_float2(sv.x, df.x));
-    const float4 o1 = fir8_step(fir, make_float2(sv.y, df.y));
-    if (p >= 5) {  // column-filtered rows 2p-10, 2p-9 = pair p-5
+    const float4 o0 = fir8_step<2 * UU>(fir, p0);
+    const float4 o1 = fir8_step<2 * UU + 1>(fir, p1);
+    if constexpr (!FIRST) {  // column-filtered rows 2p-10, 2p-9 = pair p-5
       if (p - 5 >= k8Ring) nbar_sync(k8BarDrained + vs_slot, k8BarCount);
       const uint32_t d = vb_st + vs_off;
       sts8_f32x4(d, o0);
@@ -541,12 +577,40 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
         vs_off = 0;
       }
     }
-    if ((p & 3) == 3) {
-      sse += (double)sse_f;
-      sse_f = 0.f;
-    }
+  };
+  // Straight-line groups of five pairs (ten rows = one turn of the FIR slots; no
+  // branch between the steps, so the 40 state registers keep their places):
+  // group 0 without ring writes, whole groups, then the npairs % 5 tail.
+  // H >= 11 rows, so there are at least six pairs.
+  auto flush_sse = [&]() {
+    sse += (double)sse_f;  // ten squared differences per float32 partial
+    sse_f = 0.f;
+  };
+  pair_step(PairIdx8<0>{}, PairIdx8<1>{}, 0);
+  pair_step(PairIdx8<1>{}, PairIdx8<1>{}, 1);
+  pair_step(PairIdx8<2>{}, PairIdx8<1>{}, 2);
+  pair_step(PairIdx8<3>{}, PairIdx8<1>{}, 3);
+  pair_step(PairIdx8<4>{}, PairIdx8<1>{}, 4);
+  flush_sse();
+  const int ngroups = npairs / 5;
+#pragma unroll 1
+  for (int gi = 1; gi < ngroups; ++gi) {
+    const int p0 = 5 * gi;
+    pair_step(PairIdx8<0>{}, PairIdx8<0>{}, p0);
+    pair_step(PairIdx8<1>{}, PairIdx8<0>{}, p0 + 1);
+    pair_step(PairIdx8<2>{}, PairIdx8<0>{}, p0 + 2);
+    pair_step(PairIdx8<3>{}, PairIdx8<0>{}, p0 + 3);
+    pair_step(PairIdx8<4>{}, PairIdx8<0>{}, p0 + 4);
+    flush_sse();
   }
-  sse += (double)sse_f;
+  {
+    const int p0 = 5 * ngroups, rem = npairs - p0;
+    if (rem > 0) pair_step(PairIdx8<0>{}, PairIdx8<0>{}, p0);
+    if (rem > 1) pair_step(PairIdx8<1>{}, PairIdx8<0>{}, p0 + 1);
+    if (rem > 2) pair_step(PairIdx8<2>{}, PairIdx8<0>{}, p0 + 2);
+    if (rem > 3) pair_step(PairIdx8<3>{}, PairIdx8<0>{}, p0 + 3);
+    flush_sse();
+  }
   flag_warp(args.err, (qor & ~args.Li) != 0u, CV_FLAG_INT_RANGE);
 
   // deterministic CTA reduction: per band, fixed order over warps and lanes

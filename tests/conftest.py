@@ -49,7 +49,7 @@ def variant_sel():
     """Select kernel variants (cv_set_variant) for one test; restores the defaults."""
     from paper_2506_19656_b200 import _lib
 
-    defaults = {"gram_tiles": 0, "gram_nt": 64, "proj_nopf": 0, "qp_px1": 0, "qp_runtime_c": 0,
+    defaults = {"gram_tiles": 0, "gram_nt": 64, "proj_nopf": 0, "proj12": 1, "gram_checks": 0, "gram12": 1, "qp_px1": 0, "qp_runtime_c": 0,
                 "eval_kernel": 0}
 
     def sel(variants: dict):

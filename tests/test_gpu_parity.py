@@ -410,7 +410,8 @@ def test_psnr_stream_kernel(cuda, shape, B, u16):
 
 @pytest.mark.parametrize("C", [1, 5, 7, 12])
 @pytest.mark.parametrize("n_pix", [1, 63, 64 * 5 + 3, 100_003])
-@pytest.mark.parametrize("variant", [{}, {"gram_nt": 256}, {"gram_tiles": 1}])
+@pytest.mark.parametrize("variant", [{}, {"gram12": 0}, {"gram12": 0, "gram_checks": 1}, {"gram12": 0, "gram_nt": 256},
+                                     {"gram_tiles": 1}])
 def test_gram_kernels_ragged(cuda, variant_sel, C, n_pix, variant):
     """k_gram_px (64- and 256-thread CTAs) and the tiled k_gram against a float64
     numpy shifted Gram (transform.py:177-179 restated as one-pass sums): ragged
@@ -489,7 +490,7 @@ def test_ssim_bulk_kernel_shapes(cuda, variant_sel, shape, bits, n_pcs, noisy, k
 
 # ------------------------------------------------------------------ kernel variants agree bit for bit
 
-@pytest.mark.parametrize("variant", [{"qp_runtime_c": 1}, {"qp_px1": 1}, {"proj_nopf": 1}])
+@pytest.mark.parametrize("variant", [{"qp_runtime_c": 1}, {"qp_px1": 1}, {"proj12": 0}, {"proj12": 0, "proj_nopf": 1}])
 @pytest.mark.parametrize("shape,n_pcs,bits", [((3, 40, 72, 12), 6, 16), ((2, 33, 64, 12), 9, 12)])
 def test_pca_variants_bit_identical(cuda, variant_sel, variant, shape, n_pcs, bits):
     """The compile-time C = 12 PCA quantiser, the pixel-pair path and the prefetching
