@@ -443,9 +443,15 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
       if (it < nit) {
         const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
         float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
+        const float4 *g = reinterpret_cast<const float4 *>(src) + v0;
+        if (v0 - i + kG12Conv * kG12K <= nvec) {  // whole chunk inside the cube
 #pragma unroll
-        for (int k = 0; k < kG12K; ++k)
-          if (v0 + kG12Conv * k < nvec) gram_cp_async16(st + kG12Conv * k, reinterpret_cast<const float4 *>(src) + v0 + kG12Conv * k);
+          for (int k = 0; k < kG12K; ++k) gram_cp_async16(st + kG12Conv * k, g + kG12Conv * k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kG12K; ++k)
+            if (v0 + kG12Conv * k < nvec) gram_cp_async16(st + kG12Conv * k, g + kG12Conv * k);
+        }
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
@@ -459,14 +465,17 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
       const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
       const float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
       double *tile = tiles + (size_t)bf * (kG12Px * kG12PxStride);
+      if (v0 - i + kG12Conv * kG12K <= nvec) {
+        // whole chunk inside the cube: four independent vectors, no branches
+        float4 x[kG12K];
 #pragma unroll
-      for (int k = 0; k < kG12K; ++k) {
-        const int vl = i + kG12Conv * k;       // vector inside the chunk: pixel vl / 3, bands 4 r ..
-        double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
-        double d[4] = {0.0, 0.0, 0.0, 0.0};
-        if (v0 + kG12Conv * k < nvec) {
-          const float4 x = st[kG12Conv * k];
-          const float xv[4] = {x.x, x.y, x.z, x.w};
+        for (int k = 0; k < kG12K; ++k) x[k] = st[kG12Conv * k];
+#pragma unroll
+        for (int k = 0; k < kG12K; ++k) {
+          const int vl = i + kG12Conv * k;  // vector inside the chunk: pixel vl / 3, bands 4 r ..
+          double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
+          const float xv[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+          double d[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             mn[j] = fminf(mn[j], xv[j]);
@@ -474,9 +483,29 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
             d[j] = __dsub_rn((double)xv[j], shd[j]);
             bs[j] = __dadd_rn(bs[j], d[j]);
           }
+          *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
+          *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
         }
-        *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
-        *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kG12K; ++k) {
+          const int vl = i + kG12Conv * k;
+          double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
+          double d[4] = {0.0, 0.0, 0.0, 0.0};
+          if (v0 + kG12Conv * k < nvec) {
+            const float4 x = st[kG12Conv * k];
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              mn[j] = fminf(mn[j], xv[j]);
+              mx[j] = fmaxf(mx[j], xv[j]);
+              d[j] = __dsub_rn((double)xv[j], shd[j]);
+              bs[j] = __dadd_rn(bs[j], d[j]);
+            }
+          }
+          *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
+          *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
+        }
       }
       g12_bar_arrive(kG12BarFull + bf);
     }
@@ -857,11 +886,12 @@ k_pca_project12(const float *__restrict__ src, int64_t n_pix, TO *__restrict__ o
         a1 = __fma_rn(d1[c], w, a1);
       }
       if (j == 0) bad |= !isfinite(a0) || (v1 && !isfinite(a1));
-      mn[j] = fmin(mn[j], a0);
-      mx[j] = fmax(mx[j], a0);
+      // compare-select (a NaN never wins, like fmin / fmax, at a third of their instructions)
+      mn[j] = a0 < mn[j] ? a0 : mn[j];
+      mx[j] = a0 > mx[j] ? a0 : mx[j];
       if (v1) {
-        mn[j] = fmin(mn[j], a1);
-        mx[j] = fmax(mx[j], a1);
+        mn[j] = a1 < mn[j] ? a1 : mn[j];
+        mx[j] = a1 > mx[j] ? a1 : mx[j];
       }
       if (out) {
         out[(a * n_pix + pix) * KE + j] = (TO)a0;

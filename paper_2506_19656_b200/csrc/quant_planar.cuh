@@ -97,7 +97,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   }
   double *wsm = reinterpret_cast<double *>(qtab32 + kMaxC);  // [12][12] weights, [12] means, [12] K
   if constexpr (PX2 && PCA && CX == kQP12) {
-    for (int i = tid; i < E * kQP12; i += NT) wsm[i] = pca.W[(i / kQP12) * kMaxC + i % kQP12];
+    for (int i = tid; i < kQP12 * kQP12; i += NT) wsm[i] = i < E * kQP12 ? pca.W[(i / kQP12) * kMaxC + i % kQP12] : 0.0;
     if (tid < kQP12) wsm[kQP12 * kQP12 + tid] = pca.mean[tid];
     for (int j = tid; j < E; j += NT) wsm[kQP12 * kQP12 + kQP12 + j] = __ddiv_rn(qtab[j].L, qtab[j].s);
   }
@@ -193,31 +193,39 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
         }
         uint32_t l0 = 0, l1 = 0, badi = 0;
 #pragma unroll
-        for (int pl = 0; pl < kQP12; ++pl) {
-          if (pl < 3 * args.G) {
-            uint32_t q0, q1;
-            if (pl < E) {
-              double a0 = 0.0, a1 = 0.0;
+        for (int g = 0; g < kQP12 / 3; ++g) {
+          if (g < args.G) {
+            // the three components of a video together: six independent fma chains
+            double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-              for (int c = 0; c < kQP12; ++c) {
-                const double w = lds_f64_q(wb + 8u * (uint32_t)(pl * kQP12 + c));
-                a0 = __fma_rn(d0[c], w, a0);
-                a1 = __fma_rn(d1[c], w, a1);
+            for (int c = 0; c < kQP12; ++c) {
+#pragma unroll
+              for (int jp = 0; jp < 3; ++jp) {
+                const double w = lds_f64_q(wb + 8u * (uint32_t)((3 * g + jp) * kQP12 + c));
+                a0[jp] = __fma_rn(d0[c], w, a0[jp]);
+                a1[jp] = __fma_rn(d1[c], w, a1[jp]);
               }
-              const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
-              const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8), bs = lds_f64_q(bq + 16), bL = lds_f64_q(bq + 32);
-              const double bK = lds_f64_q(wb + 8u * (uint32_t)(kQP12 * kQP12 + kQP12 + pl));
-              q0 = quantize_pc(a0, bm, bM, bs, bK, bL, badi);
-              q1 = quantize_pc(a1, bm, bM, bs, bK, bL, badi);
-              l0 = q0;
-              l1 = q1;
-            } else {
-              const bool rep = args.pad_mode == CV_PAD_REPEAT;
-              q0 = rep ? l0 : 0u;
-              q1 = rep ? l1 : 0u;
             }
-            *reinterpret_cast<W2 *>(op) = (W2)(q0 | (q1 << (8 * sizeof(TOut))));
-            op += (pl % 3 == 2) ? gjump : HW;
+#pragma unroll
+            for (int jp = 0; jp < 3; ++jp) {
+              const int pl = 3 * g + jp;
+              uint32_t q0, q1;
+              if (pl < E) {
+                const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
+                const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8), bs = lds_f64_q(bq + 16), bL = lds_f64_q(bq + 32);
+                const double bK = lds_f64_q(wb + 8u * (uint32_t)(kQP12 * kQP12 + kQP12 + pl));
+                q0 = quantize_pc(a0[jp], bm, bM, bs, bK, bL, badi);
+                q1 = quantize_pc(a1[jp], bm, bM, bs, bK, bL, badi);
+                l0 = q0;
+                l1 = q1;
+              } else {
+                const bool rep = args.pad_mode == CV_PAD_REPEAT;
+                q0 = rep ? l0 : 0u;
+                q1 = rep ? l1 : 0u;
+              }
+              *reinterpret_cast<W2 *>(op) = (W2)(q0 | (q1 << (8 * sizeof(TOut))));
+              op += jp == 2 ? gjump : HW;
+            }
           }
         }
         bad |= badi != 0u;

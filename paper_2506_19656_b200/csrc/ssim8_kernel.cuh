@@ -55,7 +55,7 @@ constexpr int k8PcaMax = 12;
 constexpr int k8LutMax = 1024;
 constexpr int k8VbBand = 144;                    // float4 per band row (136 used + skew)
 constexpr int k8VbRow = k8GB * k8VbBand;         // float4 per filtered row (4 bands)
-constexpr int k8Bars = 64;                       // bytes of mbarriers
+constexpr int k8Bars = 128;                      // bytes of mbarriers: full_in[3] at 0, drained[6] at 64
 constexpr int k8Desc = k8GB * 16;                // bytes of the per-band SSIM constants (c0, C1, C2)
 constexpr int k8Coef = k8GB * k8PcaMax * 4;      // bytes of the inverse-PCA coefficients [band][plane]
 // Named barriers (ids 1 .. 15; no polling anywhere except the copies' mbarrier):
@@ -253,6 +253,8 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   const double L = args.L;
 
   if (threadIdx.x < k8NSMax) mbar_init8(full_in + 8 * threadIdx.x, 1);  // the loader's expect_tx arrival + bytes
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + k8Ring)
+    mbar_init8(s0 + 64 + 8 * (threadIdx.x - 32), 2 * k8GB);  // one arrival per (row, band) task of the pair
   if (threadIdx.x < k8GB) {  // per-band SSIM constants for the horizontal warps
     const double pk = (int)threadIdx.x < nb ? args.peaks[a * C + g * k8GB + threadIdx.x] : 1.0;
     reinterpret_cast<float4 *>(smem + geo.off_desc)[threadIdx.x] =
@@ -394,7 +396,10 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
           }
           hs4 += ts;
         }
-        if (e + k8Ring < nfe) nbar_arrive(k8BarDrained + slot, k8BarCount);
+        if (e + k8Ring < nfe) {  // the slot will be refilled: one arrival per task, by lane 0 after the warp's reads
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(s0 + 64u + 8u * (uint32_t)slot) : "memory");
+        }
 #pragma unroll
         for (int bq = 0; bq < k8GB; ++bq)
           if (bb == bq) hsumb[bq] += (double)hs4;
@@ -473,6 +478,7 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   uint32_t in_ph = 0;     // parity of its "copies landed" completion
   int vs_slot = 0;        // ring slot of the next filtered pair
   uint32_t vs_off = 0;    // its byte offset
+  uint32_t dr_par = 1;    // parity of the slot's "drained" completion (first reuse waits for phase 0)
   // one row pair; UU = pair index mod 5 (the FIR slots of its rows are 2 UU, 2 UU + 1)
   // FIRST: pairs 0 .. 4, whose filtered rows do not exist yet (no ring writes)
   auto pair_step = [&](auto uu, auto first, const int p) {
@@ -566,7 +572,7 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
     const float4 o0 = fir8_step<2 * UU>(fir, p0);
     const float4 o1 = fir8_step<2 * UU + 1>(fir, p1);
     if constexpr (!FIRST) {  // column-filtered rows 2p-10, 2p-9 = pair p-5
-      if (p - 5 >= k8Ring) nbar_sync(k8BarDrained + vs_slot, k8BarCount);
+      if (p - 5 >= k8Ring) mbar_wait8(bars + 64u + 8u * (uint32_t)vs_slot, dr_par);
       const uint32_t d = vb_st + vs_off;
       sts8_f32x4(d, o0);
       sts8_f32x4(d + k8VbRow * 16u, o1);
@@ -575,6 +581,7 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
       if (++vs_slot == k8Ring) {
         vs_slot = 0;
         vs_off = 0;
+        dr_par ^= 1u;
       }
     }
   };
