@@ -72,7 +72,7 @@ unsigned long long cv_launch_count(void);
  * before launching, not concurrently with launches). Names: "gram_tiles" (0/1),
  * "gram_nt" (64 or 256), "gram_checks" (0/1), "gram12" (0/1), "proj_nopf" (0/1), "proj12" (0/1), "qp_px1" (0/1),
  * "qp_runtime_c" (0/1),
- * "eval_kernel" (0 = by decode mode, 7 / 8 = force k_eval_ssim7 / k_eval_ssim8).
+ * "eval_kernel" (0 / 8 = k_eval_ssim8, the default; 7 = k_eval_ssim7).
  * Defaults are the measured-fastest variants. Unknown names / values: CV_ERR_ARG. */
 int cv_set_variant(const char *name, int value);
 

@@ -28,7 +28,7 @@ struct Variants {
   int gram_checks = 0;   // 1: per-element finite tests in k_gram_px (else NaN / inf are read off the sums)
   int qp_px1 = 0;        // 1: one pixel per thread in k_quantize_planar
   int qp_runtime_c = 0;  // 1: runtime band count for the C = 12 PCA quantiser
-  int eval_kernel = 0;   // SSIM kernel: 0 = by decode mode (PCA: k_eval_ssim8, else k_eval_ssim7), 7 / 8 = forced
+  int eval_kernel = 0;   // SSIM kernel: 0 / 8 = k_eval_ssim8 (default), 7 = k_eval_ssim7
 };
 extern Variants g_variants;
 

@@ -72,11 +72,11 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
     const int wpc = a.C < kSsimWarpsPerCta ? a.C : kSsimWarpsPerCta;
     dim3 grid((unsigned)(a.nstrips * ncg), (unsigned)a.T, (unsigned)n);
     if constexpr ((RS == RS_FRAMES_U8 || RS == RS_FRAMES_U16) && std::is_same<TO, float>::value) {
-      // PCA streams run k_eval_ssim8 (park-only rings: config 5 eval 74 -> 71 ms), the
-      // lookup-table / float64 decodes k_eval_ssim7 (its raw-input prefetch hides the
-      // dependent code -> table loads: config 2 eval 24.6 vs 27 ms); "eval_kernel" forces one
+      // k_eval_ssim8 (mbarrier-handed rings, 5-pair straight-line vertical loop) is the default
+      // for every decode mode (config 5 eval 58.8 ms, config 2 23.4 vs 24.6 ms for k_eval_ssim7);
+      // "eval_kernel" = 7 forces the older kernel for A/B runs
       const int ek = g_variants.eval_kernel;
-      if (a.ssim7 && (ek == 8 || (ek == 0 && pca))) {
+      if (a.ssim7 && ek != 7) {
         constexpr int fsz = RS == RS_FRAMES_U8 ? 1 : 2;
         const int ngrp = (a.C + k8GB - 1) / k8GB;
         dim3 g8((unsigned)(ssim8_strips(a.W) * ngrp), (unsigned)a.T, (unsigned)n);

@@ -28,11 +28,9 @@
 //     mbarrier-tracked bulk copies (cp.async.bulk, the TMA path), one per
 //     original row segment (all C bands of 128 pixels) and per frame-plane row
 //     segment, as far ahead as the ring (3 row pairs) allows.
-// Both rings are handed over with hardware named barriers (bar.arrive by one
-// side, bar.sync by the other): a waiting warp is parked by the barrier unit and
-// issues nothing, unlike an mbarrier try_wait loop (27 % of the issued
-// instructions of k_eval_ssim7 are such polls). Only the copies' completion is
-// an mbarrier. Gaussian weights are compile-time immediates.
+// The filtered-row ring is handed over through mbarriers in both directions (see
+// "Hand-offs" below), the input stages are released to the loader through named
+// barriers. Gaussian weights are compile-time immediates.
 #pragma once
 #include "eval_kernel.cuh"
 #include "ssim_kernel.cuh"
@@ -55,22 +53,21 @@ constexpr int k8PcaMax = 12;
 constexpr int k8LutMax = 1024;
 constexpr int k8VbBand = 144;                    // float4 per band row (136 used + skew)
 constexpr int k8VbRow = k8GB * k8VbBand;         // float4 per filtered row (4 bands)
-constexpr int k8Bars = 128;                      // bytes of mbarriers: full_in[3] at 0, drained[6] at 64
+constexpr int k8Bars = 192;                      // bytes of mbarriers: full_in[3] at 0, drained[6] at 64, filled[6] at 128
 constexpr int k8Desc = k8GB * 16;                // bytes of the per-band SSIM constants (c0, C1, C2)
 constexpr int k8Coef = k8GB * k8PcaMax * 4;      // bytes of the inverse-PCA coefficients [band][plane]
-// Named barriers (ids 1 .. 15; no polling anywhere except the copies' mbarrier):
-//   k8BarFilled + slot   the 16 vertical warps arrive, the 8 horizontal workers
-//                        of the pair's (row, band) tasks wait parked;
-//   k8BarDrained + slot  those 8 workers arrive, the vertical warps wait parked
-//                        before they overwrite the slot (this puts the vertical
-//                        warps in step once per pair; an mbarrier each warp polls
-//                        on its own measured the same time at 40 % more issued
-//                        instructions, the polls competing with the workers);
-//   k8BarStage + stage   the vertical warps arrive when they have read an input
-//                        stage, the loader waits parked before refilling it.
-constexpr int k8BarFilled = 1, k8BarDrained = 1 + k8Ring, k8BarStage = 1 + 2 * k8Ring;
+// Hand-offs:
+//   filled[slot]   mbarrier, one arrival per vertical warp (lane 0 after __syncwarp);
+//                  a horizontal worker waits for it alone (try_wait suspends the warp in
+//                  hardware). As a named barrier (bar.sync over 16 + 8 warps) it completed
+//                  only when ALL eight workers of the pair had reached it, so the workers ran
+//                  pair by pair in step, three of the eleven idle: 68.7 -> 58.8 ms on config 5.
+//   drained[slot]  mbarrier, one arrival per (row, band) task; a vertical warp waits for it
+//                  on its own before it overwrites the slot (no vertical-vertical lock-step).
+//   k8BarStage + stage   named barrier: the vertical warps arrive when they have read an
+//                  input stage, the loader waits parked before refilling it.
+constexpr int k8BarStage = 1;
 static_assert(k8BarStage + k8NSMax <= 16, "named barrier ids");
-constexpr int k8BarCount = 32 * (k8VW + 2 * k8GB);
 enum { K8_LUT = 0, K8_F64 = 1, K8_PCA = 2 };
 
 __host__ __device__ inline int ssim8_strips(int64_t W) { return (int)((W - 2 * kSsimRadius + k8Out - 1) / k8Out); }
@@ -126,6 +123,18 @@ __device__ __forceinline__ void mbar_wait8(uint32_t b, uint32_t parity) {
         : "r"(b), "r"(parity)
         : "memory");
   }
+}
+// try_wait suspends the thread in hardware for a bounded time; looping on it is
+// the nearest thing to a parked wait an mbarrier offers
+__device__ __forceinline__ void mbar_wait8_suspend(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n}\n" ::"r"(b), "r"(parity)
+      : "memory");
 }
 // global -> shared bulk copy (TMA engine), completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s8(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
@@ -255,6 +264,8 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   if (threadIdx.x < k8NSMax) mbar_init8(full_in + 8 * threadIdx.x, 1);  // the loader's expect_tx arrival + bytes
   if (threadIdx.x >= 32 && threadIdx.x < 32 + k8Ring)
     mbar_init8(s0 + 64 + 8 * (threadIdx.x - 32), 2 * k8GB);  // one arrival per (row, band) task of the pair
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + k8Ring)
+    mbar_init8(s0 + 128 + 8 * (threadIdx.x - 64), k8VW);  // one arrival per vertical warp
   if (threadIdx.x < k8GB) {  // per-band SSIM constants for the horizontal warps
     const double pk = (int)threadIdx.x < nb ? args.peaks[a * C + g * k8GB + threadIdx.x] : 1.0;
     reinterpret_cast<float4 *>(smem + geo.off_desc)[threadIdx.x] =
@@ -356,7 +367,7 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
       for (int k = h; k < ntask; k += k8HWork) {
         const int e = k >> 3, hsub = (k >> 2) & 1, bb = k & 3;
         const int slot = e % k8Ring;
-        nbar_sync(k8BarFilled + slot, k8BarCount);
+        mbar_wait8_suspend(s0 + 128u + 8u * (uint32_t)slot, (uint32_t)((e / k8Ring) & 1));
         if (bb < nb && hv_any && 2 * e + hsub <= H32 - kSsimTaps) {
           const float4 cc = lds8_f32x4(cst + 16u * (uint32_t)bb);
           const uint32_t hv = vb + 16u * (uint32_t)(vb8_skew(bb) + lane) + (uint32_t)slot * kVbPair +
@@ -576,7 +587,8 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
       const uint32_t d = vb_st + vs_off;
       sts8_f32x4(d, o0);
       sts8_f32x4(d + k8VbRow * 16u, o1);
-      nbar_arrive(k8BarFilled + vs_slot, k8BarCount);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bars + 128u + 8u * (uint32_t)vs_slot) : "memory");
       vs_off += kVbPair;
       if (++vs_slot == k8Ring) {
         vs_slot = 0;
