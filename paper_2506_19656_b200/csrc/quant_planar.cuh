@@ -55,7 +55,7 @@ __device__ __forceinline__ double lds_f64_q(uint32_t a) {
 // the reference's own operation order decides.
 // No clamping here (the launcher sends clamped streams to the generic kernel);
 // out-of-range / NaN values set `bad` (transform.py:92-97 raises).
-__device__ __forceinline__ uint32_t quantize_pc(double v, double m, double M, double s, double K, double L,
+__device__ __forceinline__ uint32_t quantize_pc(double v, double m, double M, uint32_t sl_addr, double K,
                                                 uint32_t &bad) {
   if (!(v >= m && v <= M)) bad = 1u;
   const double diff = __dsub_rn(v, m);
@@ -63,7 +63,10 @@ __device__ __forceinline__ uint32_t quantize_pc(double v, double m, double M, do
   double q = floor(t);
   const double fr = __dsub_rn(t, q);
   const double eps = 3.725290298461914e-09;  // 2^-28
-  if (fr < eps || fr > 1.0 - eps) q = floor(__dadd_rn(__dmul_rn(__ddiv_rn(diff, s), L), 0.5));
+  if (fr < eps || fr > 1.0 - eps) {  // rare: span and L are only loaded here
+    const double s = lds_f64_q(sl_addr), L = lds_f64_q(sl_addr + 16);
+    q = floor(__dadd_rn(__dmul_rn(__ddiv_rn(diff, s), L), 0.5));
+  }
   return min((uint32_t)q, 65535u);  // a constant band has span 1 and v = m: t = 0.5, q = 0
 }
 
@@ -185,11 +188,27 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
         const uint32_t wb = (uint32_t)__cvta_generic_to_shared(wsm);
         const uint32_t qb = (uint32_t)__cvta_generic_to_shared(qtab);
         double d0[kQP12], d1[kQP12];
+        if constexpr (std::is_same<TIn, float>::value) {
+          // the pair's 24 floats as six 16-byte loads (p is even: 96-byte aligned)
+          float xv[2 * kQP12];
 #pragma unroll
-        for (int c = 0; c < kQP12; ++c) {
-          const double mu = lds_f64_q(wb + 8u * (kQP12 * kQP12 + c));
-          d0[c] = __dsub_rn((double)px[c], mu);
-          d1[c] = __dsub_rn((double)px[kQP12 + c], mu);
+          for (int q4 = 0; q4 < 2 * kQP12 / 4; ++q4) {
+            const float4 v4 = *reinterpret_cast<const float4 *>(px + 4 * q4);
+            xv[4 * q4] = v4.x, xv[4 * q4 + 1] = v4.y, xv[4 * q4 + 2] = v4.z, xv[4 * q4 + 3] = v4.w;
+          }
+#pragma unroll
+          for (int c = 0; c < kQP12; ++c) {
+            const double mu = lds_f64_q(wb + 8u * (kQP12 * kQP12 + c));
+            d0[c] = __dsub_rn((double)xv[c], mu);
+            d1[c] = __dsub_rn((double)xv[kQP12 + c], mu);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < kQP12; ++c) {
+            const double mu = lds_f64_q(wb + 8u * (kQP12 * kQP12 + c));
+            d0[c] = __dsub_rn((double)px[c], mu);
+            d1[c] = __dsub_rn((double)px[kQP12 + c], mu);
+          }
         }
         uint32_t l0 = 0, l1 = 0, badi = 0;
 #pragma unroll
@@ -212,10 +231,10 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
               uint32_t q0, q1;
               if (pl < E) {
                 const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
-                const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8), bs = lds_f64_q(bq + 16), bL = lds_f64_q(bq + 32);
+                const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8);
                 const double bK = lds_f64_q(wb + 8u * (uint32_t)(kQP12 * kQP12 + kQP12 + pl));
-                q0 = quantize_pc(a0[jp], bm, bM, bs, bK, bL, badi);
-                q1 = quantize_pc(a1[jp], bm, bM, bs, bK, bL, badi);
+                q0 = quantize_pc(a0[jp], bm, bM, bq + 16, bK, badi);
+                q1 = quantize_pc(a1[jp], bm, bM, bq + 16, bK, badi);
                 l0 = q0;
                 l1 = q1;
               } else {

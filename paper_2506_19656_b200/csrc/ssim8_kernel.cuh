@@ -41,12 +41,12 @@ constexpr int k8Cols = 128;
 constexpr int k8Out = k8Cols - 2 * kSsimRadius;  // 118
 constexpr int k8GB = 4;                          // bands per CTA
 constexpr int k8VW = 16;                         // vertical warps (warpgroups 0-3)
-constexpr int k8HW = 12;                         // horizontal warpgroups' warps (4-6): 11 workers + the loader
+constexpr int k8HW = 16;                         // horizontal warpgroups' warps (4-7): 15 workers + the loader
 constexpr int k8HWork = k8HW - 1;
 constexpr int k8Threads = 32 * (k8VW + k8HW);
 constexpr int k8RegsV = 88;                      // setmaxnreg: vertical warpgroups
-constexpr int k8RegsH = 48;                      // setmaxnreg: horizontal warpgroups
-constexpr int k8NSMax = 3;                       // input ring stages (row pairs); 16 barrier ids bound it
+constexpr int k8RegsH = 40;                      // setmaxnreg: horizontal warpgroups (512 x 88 + 512 x 40 = the register file)
+constexpr int k8NSMax = 5;                       // input ring stages (row pairs)
 constexpr int k8SmemMax = 227 * 1024;
 constexpr int k8Ring = 6;                        // filtered-row ring slots (row pairs); even
 constexpr int k8PcaMax = 12;
@@ -56,6 +56,7 @@ constexpr int k8VbRow = k8GB * k8VbBand;         // float4 per filtered row (4 b
 constexpr int k8Bars = 192;                      // bytes of mbarriers: full_in[3] at 0, drained[6] at 64, filled[6] at 128
 constexpr int k8Desc = k8GB * 16;                // bytes of the per-band SSIM constants (c0, C1, C2)
 constexpr int k8Coef = k8GB * k8PcaMax * 4;      // bytes of the inverse-PCA coefficients [band][plane]
+constexpr int k8HsBytes = k8HW * 32 * k8GB * 8;  // per-thread float64 SSIM sums of the horizontal warps [thread][band]
 // Hand-offs:
 //   filled[slot]   mbarrier, one arrival per vertical warp (lane 0 after __syncwarp);
 //                  a horizontal worker waits for it alone (try_wait suspends the warp in
@@ -73,7 +74,7 @@ enum { K8_LUT = 0, K8_F64 = 1, K8_PCA = 2 };
 __host__ __device__ inline int ssim8_strips(int64_t W) { return (int)((W - 2 * kSsimRadius + k8Out - 1) / k8Out); }
 
 struct Ssim8Geom {
-  int ob, fb, np, ns, stage, off_desc, off_coef, off_in, off_vb, off_lut, total;
+  int ob, fb, np, ns, stage, off_desc, off_coef, off_in, off_vb, off_lut, off_hs, total;
 };
 
 // shared-memory geometry: np frame planes per row (PCA: E; else the group's bands)
@@ -86,12 +87,13 @@ __host__ __device__ inline Ssim8Geom ssim8_geom(int C, int np, int fsz, bool lut
   g.off_desc = k8Bars;
   g.off_coef = g.off_desc + k8Desc;
   g.off_in = g.off_coef + k8Coef;
-  const int rest = g.off_in + k8Ring * 2 * k8VbRow * 16 + (lut ? k8GB * k8LutMax * 8 : 0);
+  const int rest = g.off_in + k8Ring * 2 * k8VbRow * 16 + (lut ? k8GB * k8LutMax * 8 : 0) + k8HsBytes;
   g.ns = (k8SmemMax - rest) / g.stage;
   g.ns = g.ns > k8NSMax ? k8NSMax : g.ns;  // < 2: the kernel cannot run (the launcher checks)
   g.off_vb = g.off_in + g.ns * g.stage;
   g.off_lut = g.off_vb + k8Ring * 2 * k8VbRow * 16;
-  g.total = g.off_lut + (lut ? k8GB * k8LutMax * 8 : 0);
+  g.off_hs = g.off_lut + (lut ? k8GB * k8LutMax * 8 : 0);
+  g.total = g.off_hs + k8HsBytes;
   return g;
 }
 
@@ -101,39 +103,17 @@ __device__ __forceinline__ void mbar_init8(uint32_t b, int count) {
 __device__ __forceinline__ void mbar_arrive_tx8(uint32_t b, uint32_t tx) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(tx) : "memory");
 }
-// One try_wait (which may suspend briefly in hardware); on failure the warp
-// sleeps before polling again instead of spinning on issue slots the working
-// warps need.
-__device__ __forceinline__ void mbar_wait8(uint32_t b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(b), "r"(parity)
-      : "memory");
-  while (!ok) {
-    asm volatile("nanosleep.u32 128;\n" ::: "memory");
-    asm volatile(
-        "{\n.reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(b), "r"(parity)
-        : "memory");
-  }
-}
 // try_wait suspends the thread in hardware for a bounded time; looping on it is
-// the nearest thing to a parked wait an mbarrier offers
-__device__ __forceinline__ void mbar_wait8_suspend(uint32_t b, uint32_t parity) {
+// the nearest thing to a parked wait an mbarrier offers (the time hint keeps the polls
+// rare: without it 13 % of the issued instructions of the kernel were polls)
+__device__ __forceinline__ void mbar_wait8(uint32_t b, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@p bra DONE_%=;\n"
       "bra WAIT_%=;\n"
-      "DONE_%=:\n}\n" ::"r"(b), "r"(parity)
+      "DONE_%=:\n}\n" ::"r"(b), "r"(parity), "r"(0x989680u)
       : "memory");
 }
 // global -> shared bulk copy (TMA engine), completion counted on `bar` in bytes
@@ -312,7 +292,10 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(k8RegsH));
     // ------------------------------------------------------------------ horizontal warpgroups
     const int h = w - k8VW;
-    double hsumb[k8GB] = {0.0, 0.0, 0.0, 0.0};  // a worker's tasks cycle through the bands
+    // a worker's tasks cycle through the bands: its four float64 sums live in shared memory
+    double *hsl = reinterpret_cast<double *>(smem + geo.off_hs) + (size_t)(h * 32 + lane) * k8GB;
+#pragma unroll
+    for (int bq = 0; bq < k8GB; ++bq) hsl[bq] = 0.0;
     if (h == k8HWork) {
       // ---------------------------------------------------------------- loader warp
       // copy k of a pair (lane k): row k / ncp of the pair, piece k % ncp
@@ -367,7 +350,7 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
       for (int k = h; k < ntask; k += k8HWork) {
         const int e = k >> 3, hsub = (k >> 2) & 1, bb = k & 3;
         const int slot = e % k8Ring;
-        mbar_wait8_suspend(s0 + 128u + 8u * (uint32_t)slot, (uint32_t)((e / k8Ring) & 1));
+        mbar_wait8(s0 + 128u + 8u * (uint32_t)slot, (uint32_t)((e / k8Ring) & 1));
         if (bb < nb && hv_any && 2 * e + hsub <= H32 - kSsimTaps) {
           const float4 cc = lds8_f32x4(cst + 16u * (uint32_t)bb);
           const uint32_t hv = vb + 16u * (uint32_t)(vb8_skew(bb) + lane) + (uint32_t)slot * kVbPair +
@@ -411,15 +394,11 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(s0 + 64u + 8u * (uint32_t)slot) : "memory");
         }
-#pragma unroll
-        for (int bq = 0; bq < k8GB; ++bq)
-          if (bb == bq) hsumb[bq] += (double)hs4;
+        hsl[bb] += (double)hs4;
         hs4 = 0.f;
       }
     }
     __syncthreads();  // the ring is idle
-#pragma unroll
-    for (int bq = 0; bq < k8GB; ++bq) red[k8VW * 32 + (h * 32 + lane) * k8GB + bq] = hsumb[bq];
     __syncthreads();  // all partials written
     return;
   }
@@ -641,7 +620,8 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
     double s1 = 0.0, s2 = 0.0;
     for (int ww = 0; ww < k8VW; ++ww)
       for (int l = bq; l < 32; l += 4) s1 += red[ww * 32 + l];
-    for (int i = 0; i < k8HW * 32; ++i) s2 += red[k8VW * 32 + i * k8GB + bq];
+    const double *hs = reinterpret_cast<const double *>(smem + geo.off_hs);
+    for (int i = 0; i < k8HW * 32; ++i) s2 += hs[i * k8GB + bq];
     double *pp = args.part + ((a * T + t) * args.nstrips + strip) * 2 * C;
     pp[g * k8GB + bq] = s1;
     pp[C + g * k8GB + bq] = s2;
