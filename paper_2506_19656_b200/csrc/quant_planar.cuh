@@ -48,27 +48,13 @@ __device__ __forceinline__ double lds_f64_q(uint32_t a) {
   return v;
 }
 
-// quantize (transform.py:98-105) of one float64 component. Fast path: one fma,
-// t = (v - m) K + 0.5 with K = RN(L / span); it differs from the reference's
-// RN(RN(RN(v - m) / span) L) + 0.5 by less than 4 L 2^-53 < 4e-11, so whenever
-// frac(t) is more than 2^-28 away from an integer both floors agree; otherwise
-// the reference's own operation order decides.
-// No clamping here (the launcher sends clamped streams to the generic kernel);
-// out-of-range / NaN values set `bad` (transform.py:92-97 raises).
-__device__ __forceinline__ uint32_t quantize_pc(double v, double m, double M, uint32_t sl_addr, double K,
-                                                uint32_t &bad) {
-  if (!(v >= m && v <= M)) bad = 1u;
-  const double diff = __dsub_rn(v, m);
-  const double t = __fma_rn(diff, K, 0.5);
-  double q = floor(t);
-  const double fr = __dsub_rn(t, q);
-  const double eps = 3.725290298461914e-09;  // 2^-28
-  if (fr < eps || fr > 1.0 - eps) {  // rare: span and L are only loaded here
-    const double s = lds_f64_q(sl_addr), L = lds_f64_q(sl_addr + 16);
-    q = floor(__dadd_rn(__dmul_rn(__ddiv_rn(diff, s), L), 0.5));
-  }
-  return min((uint32_t)q, 65535u);  // a constant band has span 1 and v = m: t = 0.5, q = 0
-}
+// C = 12 PCA path, quantize (transform.py:98-105) of a float64 component. Fast path: one
+// fma, t = (v - m) K + 0.5 with K = RN(L / span); it differs from the reference's
+// RN(RN(RN(v - m) / span) L) + 0.5 by less than 4 L 2^-53 < 4e-11, so whenever frac(t) is
+// more than 2^-28 away from an integer both floors agree; otherwise the reference's own
+// operation order decides (one branch per group of six values). A constant band has span 1
+// and v = m: t = 0.5, code 0. Clamped streams take the generic kernel; out-of-range / NaN
+// values set the RANGE flag (transform.py:92-97 raises).
 
 template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false, int CX = 0>
 __global__ void __launch_bounds__(256)
@@ -225,16 +211,50 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
                 a1[jp] = __fma_rn(d1[c], w, a1[jp]);
               }
             }
+            // fast codes of the group's six values; ONE rare branch recomputes the group in the
+            // reference's operation order when any of them is within 2^-28 of a rounding tie
+            uint32_t qq0[3], qq1[3];
+            bool near = false;
+            const double eps = 3.725290298461914e-09;  // 2^-28
+#pragma unroll
+            for (int jp = 0; jp < 3; ++jp) {
+              const int pl = 3 * g + jp;
+              qq0[jp] = qq1[jp] = 0u;
+              if (pl < E) {
+                const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
+                const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8);
+                const double bK = lds_f64_q(wb + 8u * (uint32_t)(kQP12 * kQP12 + kQP12 + pl));
+                if (!(a0[jp] >= bm && a0[jp] <= bM)) badi = 1u;
+                if (!(a1[jp] >= bm && a1[jp] <= bM)) badi = 1u;
+                const double t0 = __fma_rn(__dsub_rn(a0[jp], bm), bK, 0.5), t1 = __fma_rn(__dsub_rn(a1[jp], bm), bK, 0.5);
+                const double f0 = floor(t0), f1 = floor(t1);
+                const double r0 = __dsub_rn(t0, f0), r1 = __dsub_rn(t1, f1);
+                near |= (r0 < eps) | (r0 > 1.0 - eps) | (r1 < eps) | (r1 > 1.0 - eps);
+                qq0[jp] = min((uint32_t)f0, 65535u);
+                qq1[jp] = min((uint32_t)f1, 65535u);
+              }
+            }
+            if (near) {
+#pragma unroll
+              for (int jp = 0; jp < 3; ++jp) {
+                const int pl = 3 * g + jp;
+                if (pl < E) {
+                  const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
+                  const double bm = lds_f64_q(bq), bs = lds_f64_q(bq + 16), bL = lds_f64_q(bq + 32);
+                  const double x0 = __dmul_rn(__ddiv_rn(__dsub_rn(a0[jp], bm), bs), bL);
+                  const double x1 = __dmul_rn(__ddiv_rn(__dsub_rn(a1[jp], bm), bs), bL);
+                  qq0[jp] = min((uint32_t)floor(__dadd_rn(x0, 0.5)), 65535u);
+                  qq1[jp] = min((uint32_t)floor(__dadd_rn(x1, 0.5)), 65535u);
+                }
+              }
+            }
 #pragma unroll
             for (int jp = 0; jp < 3; ++jp) {
               const int pl = 3 * g + jp;
               uint32_t q0, q1;
               if (pl < E) {
-                const uint32_t bq = qb + (uint32_t)(pl * sizeof(QBand));
-                const double bm = lds_f64_q(bq), bM = lds_f64_q(bq + 8);
-                const double bK = lds_f64_q(wb + 8u * (uint32_t)(kQP12 * kQP12 + kQP12 + pl));
-                q0 = quantize_pc(a0[jp], bm, bM, bq + 16, bK, badi);
-                q1 = quantize_pc(a1[jp], bm, bM, bq + 16, bK, badi);
+                q0 = qq0[jp];
+                q1 = qq1[jp];
                 l0 = q0;
                 l1 = q1;
               } else {

@@ -116,8 +116,8 @@ __device__ __forceinline__ void mbar_wait8(uint32_t b, uint32_t parity) {
       "DONE_%=:\n}\n" ::"r"(b), "r"(parity), "r"(0x989680u)
       : "memory");
 }
-// (Sleeping between the workers' polls - nanosleep 400 - measured 53.7 vs 52.7 ms on config 5:
-// the tight try_wait loop stays.)
+// (Sleeping between the workers' polls measured no better: nanosleep 400 -> 53.7 ms, nanosleep 48
+// -> 53.3 ms, tight try_wait loop 53.1 ms on config 5.)
 // global -> shared bulk copy (TMA engine), completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s8(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
