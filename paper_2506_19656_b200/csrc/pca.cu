@@ -369,12 +369,16 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
 // warps per scheduler at 162 registers). Here a CTA has two roles:
 //   * 3 converter warps (96 threads): thread i owns the 16-byte vectors
 //     i + 96 k of a 128-pixel chunk (always the same four bands 4 (i % 3) ..),
-//     loaded two chunks ahead into registers, converts them to shifted float64
+//     copied with cp.async into a private 4-stage ring (only the copying
+//     thread reads them back: no CTA barrier), converts them to shifted float64
 //     once, keeps the band sums / min / max, and writes the pixel-major float64
 //     tile (stride 14 doubles: conflict-free 16-byte reads);
 //   * 4 product warps = 2 pairs x parity: a pair takes 64 pixels of the tile
 //     (two per lane), each parity half of the 78 products in registers.
 // Tiles are double-buffered and handed over with named barriers (arrive / sync).
+// (Loading the vectors two chunks ahead into registers instead of the cp.async ring freed a
+// quarter of the shared-memory traffic but measured 14.5 vs 10.9 ms: the ring keeps three
+// chunks per CTA in flight without holding registers.)
 // Same shifted sums as k_gram_px (shift = first pixel), fixed-order reductions.
 constexpr int kG12C = 12;
 constexpr int kG12Conv = 96;                 // converter threads
@@ -384,7 +388,7 @@ constexpr int kG12K = 4;                     // 16-byte vectors per converter th
 constexpr int kG12Px = kG12Conv * kG12K / 3; // 128 pixels per chunk
 constexpr int kG12Stages = 4;
 constexpr int kG12PxStride = 14;             // doubles per pixel in the tile
-constexpr int kG12Ring = 8192;  // bytes kept in front of the tiles for the end-of-kernel reduction
+constexpr int kG12Ring = kG12Stages * kG12Conv * kG12K * 16;         // bytes
 constexpr int kG12Tile = kG12Px * kG12PxStride * 8;                  // bytes
 constexpr int kG12Smem = kG12Ring + 2 * kG12Tile;
 // Tile hand-offs are named barriers (arrive / sync over the CTA's 224 threads); per-warp
@@ -420,6 +424,7 @@ __global__ void __launch_bounds__(kG12Threads, 2)
 k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ partials,
          StatsEntry *__restrict__ stats, uint32_t *err) {
   extern __shared__ __align__(16) unsigned char smem[];
+  float4 *ring = reinterpret_cast<float4 *>(smem);
   double *tiles = reinterpret_cast<double *>(smem + kG12Ring);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t nvec = n_pix * 3;  // 16-byte vectors in the cube
@@ -440,51 +445,77 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
     double bs[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) mn[j] = INFINITY, mx[j] = -INFINITY, bs[j] = 0.0;
-    // register prefetch, two chunks ahead (two buffers of kG12K 16-byte vectors; the loop is
-    // unrolled by two so both stay in registers). A shared-memory staging ring cost a quarter
-    // of the kernel's shared-memory traffic (80 % of the shared-memory bandwidth was in use).
-    auto load = [&](int64_t it, float4 (&x)[kG12K]) {
-      const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
-      const float4 *g = reinterpret_cast<const float4 *>(src) + v0;
+    auto issue = [&](int64_t it) {
+      if (it < nit) {
+        const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
+        float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
+        const float4 *g = reinterpret_cast<const float4 *>(src) + v0;
+        if (v0 - i + kG12Conv * kG12K <= nvec) {  // whole chunk inside the cube
 #pragma unroll
-      for (int k = 0; k < kG12K; ++k)
-        x[k] = (it < nit && v0 + kG12Conv * k < nvec) ? __ldg(g + kG12Conv * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 0; k < kG12K; ++k) gram_cp_async16(st + kG12Conv * k, g + kG12Conv * k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kG12K; ++k)
+            if (v0 + kG12Conv * k < nvec) gram_cp_async16(st + kG12Conv * k, g + kG12Conv * k);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    auto step = [&](int64_t it, float4 (&x)[kG12K]) {
+#pragma unroll
+    for (int s0 = 0; s0 < kG12Stages - 1; ++s0) issue(s0);
+    for (int64_t it = 0; it < nit; ++it) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kG12Stages - 2) : "memory");
+      issue(it + kG12Stages - 1);  // refills the stage this thread read one iteration ago
       const int bf = (int)(it & 1);
       if (it >= 2) g12_bar_sync(kG12BarEmpty + bf);
       const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
-      const bool full = v0 - i + kG12Conv * kG12K <= nvec;  // whole chunk inside the cube
+      const float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
       double *tile = tiles + (size_t)bf * (kG12Px * kG12PxStride);
+      if (v0 - i + kG12Conv * kG12K <= nvec) {
+        // whole chunk inside the cube: four independent vectors, no branches
+        float4 x[kG12K];
 #pragma unroll
-      for (int k = 0; k < kG12K; ++k) {
-        const int vl = i + kG12Conv * k;  // vector inside the chunk: pixel vl / 3, bands 4 r ..
-        double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
-        const float xv[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
-        const bool ok = full || v0 + kG12Conv * k < nvec;
-        double d[4];
+        for (int k = 0; k < kG12K; ++k) x[k] = st[kG12Conv * k];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (ok) {
+        for (int k = 0; k < kG12K; ++k) {
+          const int vl = i + kG12Conv * k;  // vector inside the chunk: pixel vl / 3, bands 4 r ..
+          double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
+          const float xv[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+          double d[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
             mn[j] = fminf(mn[j], xv[j]);
             mx[j] = fmaxf(mx[j], xv[j]);
+            d[j] = __dsub_rn((double)xv[j], shd[j]);
+            bs[j] = __dadd_rn(bs[j], d[j]);
           }
-          d[j] = ok ? __dsub_rn((double)xv[j], shd[j]) : 0.0;
-          bs[j] = __dadd_rn(bs[j], d[j]);
+          *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
+          *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
         }
-        *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
-        *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kG12K; ++k) {
+          const int vl = i + kG12Conv * k;
+          double *dst = tile + (vl / 3) * kG12PxStride + 4 * r;
+          double d[4] = {0.0, 0.0, 0.0, 0.0};
+          if (v0 + kG12Conv * k < nvec) {
+            const float4 x = st[kG12Conv * k];
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              mn[j] = fminf(mn[j], xv[j]);
+              mx[j] = fmaxf(mx[j], xv[j]);
+              d[j] = __dsub_rn((double)xv[j], shd[j]);
+              bs[j] = __dadd_rn(bs[j], d[j]);
+            }
+          }
+          *reinterpret_cast<double2 *>(dst) = make_double2(d[0], d[1]);
+          *reinterpret_cast<double2 *>(dst + 2) = make_double2(d[2], d[3]);
+        }
       }
       g12_bar_arrive(kG12BarFull + bf);
-      load(it + 2, x);  // this buffer's next chunk
-    };
-    float4 xa[kG12K], xb[kG12K];
-    load(0, xa);
-    load(1, xb);
-    for (int64_t it = 0; it < nit; it += 2) {
-      step(it, xa);
-      if (it + 1 < nit) step(it + 1, xb);
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       isn |= isnan(bs[j]) || isnan(shd[j]);

@@ -552,8 +552,10 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
       const float2 kpm = make_float2(1.f, -1.f), kc = make_float2(-2.f * c0, 0.f);
       p0 = __ffma2_rn(make_float2(rv.x, rv.x), kpm, __fadd2_rn(make_float2(om.x, om.x), kc));
       p1 = __ffma2_rn(make_float2(rv.y, rv.y), kpm, __fadd2_rn(make_float2(om.y, om.y), kc));
-      p0.y = __fsub_rn(p0.y, df.x);
-      p1.y = __fsub_rn(p1.y, df.y);
+      // d -= lo as a packed fma (lo * (0, -1) + p): the pair stays one FFMA2 result
+      const float2 k0m = make_float2(0.f, -1.f);
+      p0 = __ffma2_rn(make_float2(df.x, df.x), k0m, p0);
+      p1 = __ffma2_rn(make_float2(df.y, df.y), k0m, p1);
       df = make_float2(p0.y, p1.y);
     } else {
       p0 = make_float2(__fadd_rn(__fadd_rn(om.x, rv.x), -2.f * c0), df.x);
