@@ -375,7 +375,7 @@ k_gram_px(const float *__restrict__ src, int64_t n_pix, int C, double *__restric
 //     tile (stride 14 doubles: conflict-free 16-byte reads);
 //   * 4 product warps = 2 pairs x parity: a pair takes 64 pixels of the tile
 //     (two per lane), each parity half of the 78 products in registers.
-// Tiles are double-buffered and handed over with named barriers (arrive / sync).
+// Four tiles are in flight, handed over with named barriers (arrive / sync).
 // (Loading the vectors two chunks ahead into registers instead of the cp.async ring freed a
 // quarter of the shared-memory traffic but measured 14.5 vs 10.9 ms: the ring keeps three
 // chunks per CTA in flight without holding registers.)
@@ -390,11 +390,12 @@ constexpr int kG12Stages = 4;
 constexpr int kG12PxStride = 14;             // doubles per pixel in the tile
 constexpr int kG12Ring = kG12Stages * kG12Conv * kG12K * 16;         // bytes
 constexpr int kG12Tile = kG12Px * kG12PxStride * 8;                  // bytes
-constexpr int kG12Smem = kG12Ring + 2 * kG12Tile;
+constexpr int kG12Tiles = 4;  // float64 tiles in flight between the two roles (2 left both waiting on each other)
+constexpr int kG12Smem = kG12Ring + kG12Tiles * kG12Tile;
 // Tile hand-offs are named barriers (arrive / sync over the CTA's 224 threads); per-warp
 // mbarriers measured slower here (11.3 vs 10.9 ms on config 5: the polls of seven warps
 // compete with two resident CTAs' product warps).
-constexpr int kG12BarFull = 1, kG12BarEmpty = 3;
+constexpr int kG12BarFull = 1, kG12BarEmpty = 1 + kG12Tiles;
 
 __device__ __forceinline__ void g12_bar_sync(int id) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(kG12Threads) : "memory");
@@ -466,8 +467,8 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
     for (int64_t it = 0; it < nit; ++it) {
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kG12Stages - 2) : "memory");
       issue(it + kG12Stages - 1);  // refills the stage this thread read one iteration ago
-      const int bf = (int)(it & 1);
-      if (it >= 2) g12_bar_sync(kG12BarEmpty + bf);
+      const int bf = (int)(it % kG12Tiles);
+      if (it >= kG12Tiles) g12_bar_sync(kG12BarEmpty + bf);
       const int64_t v0 = (b + it * G) * (kG12Conv * kG12K) + i;
       const float4 *st = ring + (size_t)(it % kG12Stages) * (kG12Conv * kG12K) + i;
       double *tile = tiles + (size_t)bf * (kG12Px * kG12PxStride);
@@ -541,7 +542,7 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
 #pragma unroll
     for (int k = 0; k < kGpxHalf; ++k) acc[k] = 0.0;
     for (int64_t it = 0; it < nit; ++it) {
-      const int bf = (int)(it & 1);
+      const int bf = (int)(it % kG12Tiles);
       g12_bar_sync(kG12BarFull + bf);
       const double *tile = tiles + (size_t)bf * (kG12Px * kG12PxStride) + (size_t)(64 * pair + lane) * kG12PxStride;
       if (H == 0) {
@@ -551,7 +552,7 @@ k_gram12(const float *__restrict__ src, int64_t n_pix, double *__restrict__ part
         g12_products<1>(tile, acc);
         g12_products<1>(tile + 32 * kG12PxStride, acc);
       }
-      if (it + 2 < nit) g12_bar_arrive(kG12BarEmpty + bf);
+      if (it + kG12Tiles < nit) g12_bar_arrive(kG12BarEmpty + bf);
     }
 #pragma unroll
     for (int k = 0; k < kGpxHalf; ++k) isn |= isnan(acc[k]);

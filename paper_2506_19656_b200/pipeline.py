@@ -561,21 +561,23 @@ class HostStreamer:
         dec = self.dec[k][:n]
         done = torch.cuda.Event()
         done.record(comp)
-        with torch.cuda.stream(self.d2h_stream):
-            self.d2h_stream.wait_event(done)
-            for b in range(n):
-                for g in range(enc.frames.shape[1]):
+        self.d2h_stream.wait_event(done)
+        arrived = None
+        # one video slice at a time: the slice goes to the host (where the codec runs), and its
+        # decoded frames come back while the next slice is still on its way out (PCIe is full duplex)
+        for b in range(n):
+            for g in range(enc.frames.shape[1]):
+                with torch.cuda.stream(self.d2h_stream):
                     hf[b, g].copy_(enc.frames[b, g], non_blocking=True)
-            back = torch.cuda.Event()
-            back.record(self.d2h_stream)
+                    back = torch.cuda.Event()
+                    back.record(self.d2h_stream)
+                with torch.cuda.stream(self.h2d_stream):
+                    self.h2d_stream.wait_event(back)
+                    dec[b, g].copy_(hf[b, g], non_blocking=True)
+                    arrived = torch.cuda.Event()
+                    arrived.record(self.h2d_stream)
         nbytes = hf.numel() * hf.element_size()
         self.d2h_bytes += nbytes
-        # the codec runs here on the host bytes; its decoded frames come back
-        with torch.cuda.stream(self.h2d_stream):
-            self.h2d_stream.wait_event(back)
-            dec.copy_(hf, non_blocking=True)
-            arrived = torch.cuda.Event()
-            arrived.record(self.h2d_stream)
         self.h2d_bytes += nbytes
         comp.wait_event(arrived)
         return dec
