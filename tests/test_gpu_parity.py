@@ -193,6 +193,22 @@ def test_pca_rank1_and_mean_only(cuda):
     assert np.abs(pcs).max() < 1e-12
 
 
+@pytest.mark.parametrize("K", [6, 9, 4])
+@pytest.mark.parametrize("shape", [(2, 9, 13, 12), (3, 40, 72, 12)])
+def test_pca_forward_c12_vs_oracle(cuda, variant_sel, K, shape):
+    """pca_forward on 12-band float32 cubes (k_pca_project12 for K in {6, 9}, the generic
+    kernel for K = 4): float64 components against the oracle (transform.py:191-199), and
+    bit for bit against the generic kernel; odd pixel counts exercise the two-pixel tail."""
+    rng = np.random.default_rng(12 + K)
+    x = (rng.standard_normal(shape) * 10.0 ** (np.arange(12) / 4) + 2.0).astype(np.float32)
+    m = G.pca_fit(x, K)
+    pcs = G.pca_forward(x, m)
+    want = O.pca_forward(x, np.asarray(m.mean), np.asarray(m.components))
+    np.testing.assert_allclose(pcs, want, rtol=0, atol=1e-9 * np.abs(want).max())
+    variant_sel({"proj12": 0})
+    np.testing.assert_array_equal(G.pca_forward(x, m), pcs)
+
+
 # ------------------------------------------------------------------ metrics
 
 @pytest.mark.parametrize("seed", range(5))
