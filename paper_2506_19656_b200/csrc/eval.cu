@@ -111,6 +111,7 @@ static int launch_eval2(const EvalArgs &a, const PcaParams &inv, bool pca, bool 
 #define CV_S7(MODE, EP)                                                                                  \
   do {                                                                                                   \
     const size_t sm = (size_t)ssim7_geom(a.C, MODE == K7_PCA ? a.E : k7GB, fsz, MODE == K7_LUT).total;    \
+    if (sm > 227 * 1024) return fail(CV_ERR_UNSUPPORTED, "cv_eval: %d channels do not fit k_eval_ssim7's rings", a.C); \
     cudaFuncSetAttribute(k_eval_ssim7<RS, MODE, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     k_eval_ssim7<RS, MODE, EP><<<g7, k7Threads, sm, st>>>(a, inv);                                       \
   } while (0)

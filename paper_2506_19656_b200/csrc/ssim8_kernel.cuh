@@ -9,7 +9,7 @@
 // CTA = one frame t of one cube, 128 adjacent input columns x0 .. x0+127
 // (x0 = 118 s; the 118 output columns x0+5 .. x0+122 need their whole window
 // inside the strip) and a group of up to four bands g*4 .. g*4+3; it walks the
-// frame top to bottom in row pairs. 28 warps in two roles:
+// frame top to bottom in row pairs. 32 warps in two roles:
 //   * 16 "vertical" warps (88 registers); lane = (column 8w + lane/4, band
 //     lane%4): conflict-free reads of the channel-last original, 16-byte recon
 //     runs. Per row pair a lane decodes its two elements (float2 lookup table
@@ -18,16 +18,17 @@
 //     folded into the coefficients), stores the recon, adds the squared error
 //     and steps the VERTICAL 11-tap filter of (s, d) and (s^2, d^2), a
 //     transposed-form FIR on packed FFMA2 (s = x'+y', d = x-y, x' = x - peak).
-//     Column-filtered row pairs go to a 6-slot shared ring.
-//   * 11 "horizontal" warps (48 registers) take the (row, band) tasks of the
-//     filtered pairs round-robin. Lane q filters columns 4q .. 4q+13 of a row
-//     into outputs 4q .. 4q+3 (14 LDS.128, 22 FFMA2 per output) and scores
-//     them. The horizontal role is a third of the instructions: it idles on
-//     the "filled" barrier rather than making the vertical warps wait.
+//     Column-filtered row pairs go to a 5-slot shared ring.
+//   * 15 "horizontal" workers (40 registers; their float64 SSIM sums live in
+//     shared memory) take the (row, band) tasks of the filtered pairs
+//     round-robin. Lane q filters columns 4q .. 4q+13 of a row into outputs
+//     4q .. 4q+3 (14 LDS.128, 22 FFMA2 per output) and scores them. The
+//     horizontal role has slack: it waits on "filled" rather than making the
+//     vertical warps wait on "drained".
 //   * 1 loader warp (in the horizontal warpgroups) feeds the input ring:
 //     mbarrier-tracked bulk copies (cp.async.bulk, the TMA path), one per
 //     original row segment (all C bands of 128 pixels) and per frame-plane row
-//     segment, as far ahead as the ring (3 row pairs) allows.
+//     segment, as far ahead as the ring (up to 5 row pairs) allows.
 // The filtered-row ring is handed over through mbarriers in both directions (see
 // "Hand-offs" below), the input stages are released to the loader through named
 // barriers. Gaussian weights are compile-time immediates.
@@ -48,7 +49,7 @@ constexpr int k8RegsV = 88;                      // setmaxnreg: vertical warpgro
 constexpr int k8RegsH = 40;                      // setmaxnreg: horizontal warpgroups (512 x 88 + 512 x 40 = the register file)
 constexpr int k8NSMax = 5;                       // input ring stages (row pairs)
 constexpr int k8SmemMax = 227 * 1024;
-constexpr int k8Ring = 6;                        // filtered-row ring slots (row pairs); even
+constexpr int k8Ring = 5;                        // filtered-row ring slots (row pairs) = pairs per unrolled group
 constexpr int k8PcaMax = 12;
 constexpr int k8LutMax = 1024;
 constexpr int k8VbBand = 144;                    // float4 per band row (136 used + skew)
@@ -473,19 +474,31 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
   uint32_t dr_par = 1;    // parity of the slot's "drained" completion (first reuse waits for phase 0)
   // one row pair; UU = pair index mod 5 (the FIR slots of its rows are 2 UU, 2 UU + 1)
   // FIRST: pairs 0 .. 4, whose filtered rows do not exist yet (no ring writes)
-  auto pair_step = [&](auto uu, auto first, const int p) {
+  // SR ("static rings"): with ns == 5 input stages and the 5-slot filtered ring, pair p = 5 gi + UU
+  // uses stage UU and slot UU, and every phase parity is gi & 1: the ring bookkeeping (about 20
+  // uniform-datapath instructions per pair) folds into immediates.
+  auto pair_step = [&](auto uu, auto first, auto srt, const int p, const int gi) {
     constexpr int UU = decltype(uu)::value;
     constexpr bool FIRST = decltype(first)::value != 0;
-    const int U = in_st;
-    const uint32_t st = in_off;
-    const bool rel = p + ns < npairs;  // the loader refills this stage: tell it when the reads are done
-    mbar_wait8(bars + 8 * U, in_ph);
-    in_off += stage_b;
-    if (++in_st == ns) {
-      in_st = 0;
-      in_off = 0;
-      in_ph ^= 1u;
+    constexpr bool SR = decltype(srt)::value != 0;
+    int U;
+    uint32_t st;
+    if constexpr (SR) {
+      U = UU;
+      st = (uint32_t)UU * stage_b;
+      mbar_wait8(bars + 8 * UU, (uint32_t)(gi & 1));
+    } else {
+      U = in_st;
+      st = in_off;
+      mbar_wait8(bars + 8 * U, in_ph);
+      in_off += stage_b;
+      if (++in_st == ns) {
+        in_st = 0;
+        in_off = 0;
+        in_ph ^= 1u;
+      }
     }
+    const bool rel = p + ns < npairs;  // the loader refills this stage: tell it when the reads are done
     // raw inputs of the pair: original values and codes
     float2 om;
     om.x = lds8_f32(st + o_off);
@@ -565,7 +578,14 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
     sse_f = fmaf(d1, d1, fmaf(d0, d0, sse_f));
     const float4 o0 = fir8_step<2 * UU>(fir, p0);
     const float4 o1 = fir8_step<2 * UU + 1>(fir, p1);
-    if constexpr (!FIRST) {  // column-filtered rows 2p-10, 2p-9 = pair p-5
+    if constexpr (!FIRST && SR) {  // column-filtered pair p - 5 = 5 (gi - 1) + UU: slot UU, reuse gi - 1
+      if (gi >= 2) mbar_wait8(bars + 64u + 8u * UU, (uint32_t)(gi & 1));
+      const uint32_t d = vb_st + (uint32_t)UU * kVbPair;
+      sts8_f32x4(d, o0);
+      sts8_f32x4(d + k8VbRow * 16u, o1);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bars + 128u + 8u * UU) : "memory");
+    } else if constexpr (!FIRST) {  // column-filtered rows 2p-10, 2p-9 = pair p-5
       if (p - 5 >= k8Ring) mbar_wait8(bars + 64u + 8u * (uint32_t)vs_slot, dr_par);
       const uint32_t d = vb_st + vs_off;
       sts8_f32x4(d, o0);
@@ -588,31 +608,35 @@ k_eval_ssim8(const EvalArgs args, const PcaParams inv) {
     sse += (double)sse_f;  // ten squared differences per float32 partial
     sse_f = 0.f;
   };
-  pair_step(PairIdx8<0>{}, PairIdx8<1>{}, 0);
-  pair_step(PairIdx8<1>{}, PairIdx8<1>{}, 1);
-  pair_step(PairIdx8<2>{}, PairIdx8<1>{}, 2);
-  pair_step(PairIdx8<3>{}, PairIdx8<1>{}, 3);
-  pair_step(PairIdx8<4>{}, PairIdx8<1>{}, 4);
-  flush_sse();
-  const int ngroups = npairs / 5;
+  auto run_all = [&](auto srt) {
+    pair_step(PairIdx8<0>{}, PairIdx8<1>{}, srt, 0, 0);
+    pair_step(PairIdx8<1>{}, PairIdx8<1>{}, srt, 1, 0);
+    pair_step(PairIdx8<2>{}, PairIdx8<1>{}, srt, 2, 0);
+    pair_step(PairIdx8<3>{}, PairIdx8<1>{}, srt, 3, 0);
+    pair_step(PairIdx8<4>{}, PairIdx8<1>{}, srt, 4, 0);
+    flush_sse();
+    const int ngroups = npairs / 5;
 #pragma unroll 1
-  for (int gi = 1; gi < ngroups; ++gi) {
-    const int p0 = 5 * gi;
-    pair_step(PairIdx8<0>{}, PairIdx8<0>{}, p0);
-    pair_step(PairIdx8<1>{}, PairIdx8<0>{}, p0 + 1);
-    pair_step(PairIdx8<2>{}, PairIdx8<0>{}, p0 + 2);
-    pair_step(PairIdx8<3>{}, PairIdx8<0>{}, p0 + 3);
-    pair_step(PairIdx8<4>{}, PairIdx8<0>{}, p0 + 4);
-    flush_sse();
-  }
-  {
-    const int p0 = 5 * ngroups, rem = npairs - p0;
-    if (rem > 0) pair_step(PairIdx8<0>{}, PairIdx8<0>{}, p0);
-    if (rem > 1) pair_step(PairIdx8<1>{}, PairIdx8<0>{}, p0 + 1);
-    if (rem > 2) pair_step(PairIdx8<2>{}, PairIdx8<0>{}, p0 + 2);
-    if (rem > 3) pair_step(PairIdx8<3>{}, PairIdx8<0>{}, p0 + 3);
-    flush_sse();
-  }
+    for (int gi = 1; gi < ngroups; ++gi) {
+      const int p0 = 5 * gi;
+      pair_step(PairIdx8<0>{}, PairIdx8<0>{}, srt, p0, gi);
+      pair_step(PairIdx8<1>{}, PairIdx8<0>{}, srt, p0 + 1, gi);
+      pair_step(PairIdx8<2>{}, PairIdx8<0>{}, srt, p0 + 2, gi);
+      pair_step(PairIdx8<3>{}, PairIdx8<0>{}, srt, p0 + 3, gi);
+      pair_step(PairIdx8<4>{}, PairIdx8<0>{}, srt, p0 + 4, gi);
+      flush_sse();
+    }
+    {
+      const int p0 = 5 * ngroups, rem = npairs - p0;
+      if (rem > 0) pair_step(PairIdx8<0>{}, PairIdx8<0>{}, srt, p0, ngroups);
+      if (rem > 1) pair_step(PairIdx8<1>{}, PairIdx8<0>{}, srt, p0 + 1, ngroups);
+      if (rem > 2) pair_step(PairIdx8<2>{}, PairIdx8<0>{}, srt, p0 + 2, ngroups);
+      if (rem > 3) pair_step(PairIdx8<3>{}, PairIdx8<0>{}, srt, p0 + 3, ngroups);
+      flush_sse();
+    }
+  };
+  if (ns == k8Ring) run_all(PairIdx8<1>{});  // five input stages: static rings
+  else run_all(PairIdx8<0>{});
   flag_warp(args.err, (qor & ~args.Li) != 0u, CV_FLAG_INT_RANGE);
 
   // deterministic CTA reduction: per band, fixed order over warps and lanes
