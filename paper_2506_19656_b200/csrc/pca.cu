@@ -833,7 +833,7 @@ __device__ __forceinline__ double lds_f64_volatile(uint32_t a) {
 
 constexpr int kP12Threads = 256;
 
-template <typename TO, int KE>
+template <typename TO, int KE, bool OUT>
 __global__ void __launch_bounds__(kP12Threads, 2)
 k_pca_project12(const float *__restrict__ src, int64_t n_pix, TO *__restrict__ out,
                 StatsEntry *__restrict__ stats, const PcaParams pca, uint32_t *err) {
@@ -900,7 +900,7 @@ k_pca_project12(const float *__restrict__ src, int64_t n_pix, TO *__restrict__ o
         mn[j] = a1 < mn[j] ? a1 : mn[j];
         mx[j] = a1 > mx[j] ? a1 : mx[j];
       }
-      if (out) {
+      if constexpr (OUT) {  // OUT = false: the range-only pass of the pipeline (no store code, fewer registers)
         out[(a * n_pix + pix) * KE + j] = (TO)a0;
         if (v1) out[(a * n_pix + pix + kP12Threads) * KE + j] = (TO)a1;
       }
@@ -1044,10 +1044,10 @@ static int launch_project(const void *src, int64_t n_cubes, int64_t n_pix, const
         if (cap2 < 1) cap2 = 1;
         if (nb2 > cap2) nb2 = cap2;
         dim3 grid2((unsigned)(nb2 < 1 ? 1 : nb2), (unsigned)n_cubes);
-        if (p.K == 6)
-          k_pca_project12<TO, 6><<<grid2, kP12Threads, 0, st>>>((const float *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
-        else
-          k_pca_project12<TO, 9><<<grid2, kP12Threads, 0, st>>>((const float *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err);
+#define CV_P12(KK, OO) k_pca_project12<TO, KK, OO><<<grid2, kP12Threads, 0, st>>>((const float *)src, n_pix, (TO *)out, (StatsEntry *)stats, p, err)
+        if (p.K == 6) { if (out) CV_P12(6, true); else CV_P12(6, false); }
+        else { if (out) CV_P12(9, true); else CV_P12(9, false); }
+#undef CV_P12
         return check_launch("cv_pca_project(12)");
       }
     }
