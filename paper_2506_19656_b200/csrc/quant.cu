@@ -397,9 +397,19 @@ static int launch_qp(const void *src, void *out, const QuantArgs &args, const Pc
     kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
   } while (0)
   if (px2 && PCA && args.C == 12 && mv <= 8 && mv > 4 && !g_variants.qp_runtime_c && !args.clamp) {
-    auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, 8, true, 12>;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);
+#define CV_QP12(EEV)                                                                                 \
+  do {                                                                                                \
+    auto kern = k_quantize_planar<TIn, TOut, FILL, PCA, 8, true, 12, EEV>;                            \
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    kern<<<grid, NT, sm, st>>>((const TIn *)src, (TOut *)out, args, pca);                             \
+  } while (0)
+    bool done12 = false;
+    if constexpr (std::is_same<TIn, float>::value && !FILL) {  // the benchmark streams: static plane counts
+      if (args.E == 6) { CV_QP12(6); done12 = true; }
+      else if (args.E == 9) { CV_QP12(9); done12 = true; }
+    }
+    if (!done12) CV_QP12(0);
+#undef CV_QP12
     return check_launch("cv_quantize(planar)");
   }
   if (px2) {

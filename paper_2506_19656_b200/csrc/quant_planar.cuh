@@ -56,14 +56,17 @@ __device__ __forceinline__ double lds_f64_q(uint32_t a) {
 // and v = m: t = 0.5, code 0. Clamped streams take the generic kernel; out-of-range / NaN
 // values set the RANGE flag (transform.py:92-97 raises).
 
-template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false, int CX = 0>
+// EE: compile-time component count of the C = 12 PCA path (6 / 9; 0 = runtime): the plane
+// guards and pad selects (52 SEL + 68 IMAD.MOV of 731 instructions per pixel pair) fold away.
+template <typename TIn, typename TOut, bool FILL, bool PCA, int MAXV, bool PX2 = false, int CX = 0, int EE = 0>
 __global__ void __launch_bounds__(256)
 k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const QuantArgs args,
                   const PcaParams pca) {
   constexpr int VE = 16 / sizeof(TIn);  // elements per 16-byte copy
   extern __shared__ __align__(16) unsigned char smem[];
   const int NT = blockDim.x, tid = threadIdx.x;
-  const int C = CX ? CX : args.C, E = args.E;  // CX: compile-time band count (PCA, C = 12)
+  const int C = CX ? CX : args.C, E = EE ? EE : args.E;  // CX: compile-time band count (PCA, C = 12)
+  const int GG = EE ? (EE + 2) / 3 : args.G;              // videos of the stream
   const int64_t T = args.T, HW = args.HW, inner = HW * C;
   const int P = PX2 ? 2 * NT : NT;          // pixels per chunk
   const int NE = P * C;                     // elements per full chunk
@@ -199,7 +202,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
         uint32_t l0 = 0, l1 = 0, badi = 0;
 #pragma unroll
         for (int g = 0; g < kQP12 / 3; ++g) {
-          if (g < args.G) {
+          if (g < GG) {
             // the three components of a video together: six independent fma chains
             double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};
 #pragma unroll
