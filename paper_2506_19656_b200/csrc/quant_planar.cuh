@@ -66,7 +66,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   extern __shared__ __align__(16) unsigned char smem[];
   const int NT = blockDim.x, tid = threadIdx.x;
   const int C = CX ? CX : args.C, E = EE ? EE : args.E;  // CX: compile-time band count (PCA, C = 12)
-  const int GG = EE ? (EE + 2) / 3 : args.G;              // videos of the stream
+  const int GG = EE ? (EE + 2) / 3 : (CX && !PCA) ? (CX + 2) / 3 : args.G;  // videos of the stream
   const int64_t T = args.T, HW = args.HW, inner = HW * C;
   const int P = PX2 ? 2 * NT : NT;          // pixels per chunk
   const int NE = P * C;                     // elements per full chunk
@@ -136,7 +136,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
   if constexpr (PX2) obase += t0 * 3 * HW;
   if constexpr (PX2 && !PCA) {
 #pragma unroll
-    for (int c = 0; c < kQRegC; ++c) rb[c] = qtab32[c < C ? c : 0];
+    for (int c = 0; c < kQRegC; ++c) rb[c] = qtab32[c < C ? c : 0];  // C is static with CX (7: minicubes, 4: RGB+NIR)
   }
 
   for (int64_t t = t0; t < t1; ++t) {
@@ -319,7 +319,7 @@ k_quantize_planar(const TIn *__restrict__ src, TOut *__restrict__ out, const Qua
       uint32_t l0 = 0, l1 = 0;
 #pragma unroll
       for (int pl = 0; pl < 3 * ((kQRegC + 2) / 3); ++pl) {
-        if (pl < 3 * args.G) {
+        if (pl < 3 * GG) {
           const int c = pl;
           uint32_t q0, q1;
           if (c < C) {

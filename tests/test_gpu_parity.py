@@ -526,3 +526,26 @@ def test_pca_variants_bit_identical(cuda, variant_sel, variant, shape, n_pcs, bi
     b = G_pipe.encode_prep(x, spec)
     assert torch.equal(b.qmins, ma) and torch.equal(b.qmaxs, a.qmaxs)
     assert torch.equal(b.frames, fa)
+
+
+@pytest.mark.parametrize("kind", ["f32_c7_fill", "u16_c4"])
+def test_static_band_count_quantiser_bit_identical(cuda, variant_sel, kind):
+    """The compile-time band-count quantisers (7 float32 bands with fill, 4 uint16 bands) write
+    exactly the frames / filled cube of the runtime-count kernel ("qp_runtime_c")."""
+    from paper_2506_19656_b200 import synth
+
+    if kind == "f32_c7_fill":
+        x = synth.minicube(77, (9, 24, 32, 7), device=cuda)
+        spec = G_pipe.StreamSpec(10, seg_len=4)
+    else:
+        x = synth.dynamic_earthnet(78, (6, 32, 32, 4), device=cuda).contiguous()
+        spec = G_pipe.StreamSpec(8)
+    a = G_pipe.encode_prep(x, spec)
+    fa = a.frames.clone()
+    filled_a = a.filled.clone() if a.filled is not None else None
+    variant_sel({"qp_runtime_c": 1})
+    b = G_pipe.encode_prep(x, spec)
+    assert torch.equal(b.frames, fa)
+    assert torch.equal(b.qmins, a.qmins) and torch.equal(b.qmaxs, a.qmaxs)
+    if filled_a is not None:
+        assert torch.equal(b.filled, filled_a)
